@@ -1,0 +1,195 @@
+/*
+ * phylograd-b200 C-ABI — the drop-in boundary for the logL + branch-gradient
+ * hot path of phylograd (reference: /root/reference/proj/include/phylograd).
+ *
+ * The reference exposes the path as the header-only C++ class
+ * phylograd::LikelihoodEngine (engine.hpp:47-438) with no FFI.  Each entry
+ * point below replaces one piece of that class (cited per function); the C++
+ * facade in include/phylograd_b200/engine.hpp rebuilds the reference's class
+ * surface on top of these calls, and paper_1905_12146_b200/ mirrors it in
+ * Python.  Plain pointers and sizes only; all arrays are HOST memory unless a
+ * name says _device.  No CPU fallback: every compute call runs CUDA kernels on
+ * the engine's device and fails with PG_ERR_CUDA if that is impossible.
+ *
+ * Node numbering follows the reference (tree.hpp:6-8): tips 1..N, internal
+ * nodes N+1..2N-1, root 2N-1; branch i is named by its child node, output
+ * index i-1.
+ */
+#ifndef PHYLOGRAD_B200_H
+#define PHYLOGRAD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The facade rethrows them as the reference's exception types
+ * (engine.hpp:58-70, :117-120, :211-215, :226-227; tree.hpp:141-146). */
+enum pg_status {
+  PG_OK = 0,
+  PG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  PG_ERR_RUNTIME = 2,          /* std::runtime_error ("underflowed", "non-finite") */
+  PG_ERR_LOGIC = 3,            /* std::logic_error (pass ordering) */
+  PG_ERR_NEWICK = 4,           /* phylograd::NewickError (position in pg_last_error) */
+  PG_ERR_CUDA = 5,             /* device / driver failure */
+  PG_ERR_NOT_SUPPORTED = 6
+};
+
+/* Evaluation flags for pg_evaluate (engine.hpp:146-164; clock.hpp:146-152). */
+enum pg_eval_flags {
+  PG_EVAL_LOGL = 1,      /* log_likelihood() */
+  PG_EVAL_GRAD = 2,      /* branch_gradient(): d logL / d b_i */
+  PG_EVAL_HESS = 4,      /* branch_gradient(true): Hessian diagonal */
+  PG_EVAL_RATE_GRAD = 8, /* chain rule to branch rates: d logL / d r_i = dt_i * g_i (needs durations) */
+  PG_EVAL_FORCE = 16,    /* recompute even when caches are valid (invalidate_caches()) */
+  PG_EVAL_POST_PASS = 32, /* logL through the cached post-order route: post_order_pass() (engine.hpp:182) */
+  PG_EVAL_REQUIRE_POST = 64 /* pre_order_pass(): PG_ERR_LOGIC unless the post pass is current (engine.hpp:226-227) */
+};
+
+/* engine.hpp:33-37 EngineOptions + device placement. */
+typedef struct pg_options {
+  double rescaling_threshold; /* default 1e-150 */
+  int force_rescaling;        /* rescale at every internal visit */
+  int disable_rescaling;      /* never rescale (testing only) */
+  int device;                 /* CUDA ordinal */
+  int capture_partials;       /* keep per-node post/pre partials for pg_get_partials (debug, small P) */
+  int reserved[8];
+} pg_options;
+
+typedef struct pg_engine pg_engine;
+
+void pg_default_options(pg_options* opt);
+/* Thread-local text of the last failure (also after a failed pg_create). */
+const char* pg_last_error(void);
+
+/* ---- engine lifecycle (replaces the LikelihoodEngine ctor, engine.hpp:49-110).
+ * The reference holds const references to tree/alignment/model (:416-418);
+ * the C-ABI copies everything to the device instead, so callers may free
+ * their host arrays after each setter returns. */
+int pg_create(const pg_options* opt, pg_engine** out);
+void pg_destroy(pg_engine* e);
+
+/* tree.hpp:27-77: parent[2N] (parent[root]=0), children[2N][2] ({0,0} for
+ * tips), post_order[2N-1] (validated as an admissible order: children before
+ * parents, tree.hpp:81-126).  Branch lengths come from pg_set_branch_lengths. */
+int pg_set_topology(pg_engine* e, int tip_count, const int32_t* parent, const int32_t* children,
+                    const int32_t* post_order);
+
+/* alignment.hpp:129-238 + engine.hpp:64-79 (tip codes).  codes is tip-major
+ * [tip_count][pattern_count] int8 (compact tip codes; the reference keeps
+ * dense m x P tip partials, alignment.hpp:219-227): 0..m-1 = observed state,
+ * -1 = missing (all-ones partial), m+a = ambiguity class a whose partial is
+ * ambiguity[a*m .. a*m+m) (m + ambiguity_count <= 127).  weights are the
+ * integer pattern multiplicities (alignment.hpp:135). */
+int pg_set_patterns(pg_engine* e, int state_count, int pattern_count, const int8_t* codes,
+                    int ambiguity_count, const double* ambiguity, const int64_t* weights);
+
+/* substitution.hpp:81-93 raw constructor: q row-major m x m (rows sum to 0),
+ * pi root distribution.  reversible != 0 and pi > 0 builds the symmetric
+ * eigensystem (substitution.hpp:196-208); otherwise P(t) uses Pade
+ * scaling-and-squaring (substitution.hpp:155-156), both on the GPU. */
+int pg_set_model(pg_engine* e, int state_count, const double* q, const double* pi, int reversible);
+/* substitution.hpp:138-143: raw per-branch generator (non-homogeneous). */
+int pg_set_branch_generator(pg_engine* e, int branch, const double* q);
+
+/* substitution.hpp:23-51 (RateCategories::make checks). */
+int pg_set_categories(pg_engine* e, int category_count, const double* rates, const double* probs);
+
+/* engine.hpp:116-124: validates size/finiteness/sign; a bit-identical vector
+ * keeps the caches valid.  b has 2N-2 entries (index node-1). */
+int pg_set_branch_lengths(pg_engine* e, const double* b);
+/* Same, reading a DEVICE pointer (no host round trip). */
+int pg_set_branch_lengths_device(pg_engine* e, const double* b_device);
+int pg_get_branch_lengths(const pg_engine* e, double* b);
+
+/* clock.hpp:42-55 / cli.hpp:429-440: calendar durations dt_i = t_i - t_pa(i)
+ * used by PG_EVAL_RATE_GRAD (d logL / d r_i = dt_i g_i, b_i = r_i dt_i). */
+int pg_set_clock_durations(pg_engine* e, const double* dt);
+
+/* engine.hpp:146-164.  Synchronous: returns when results are in host memory.
+ * log_likelihood may be NULL; grad/hess (2N-2 doubles) may be NULL unless the
+ * matching flag is set.  With PG_EVAL_RATE_GRAD, grad receives dt_i*g_i and
+ * hess dt_i^2*H_ii. */
+int pg_evaluate(pg_engine* e, int flags, double* log_likelihood, double* grad, double* hess);
+
+/* Asynchronous variant for multi-GPU sharding: writes [logL, g(2N-2), h(2N-2)]
+ * (h only with PG_EVAL_HESS) into out_device on the engine stream; the caller
+ * all-reduces it (NCCL) and then calls pg_check_errors. */
+int pg_evaluate_device(pg_engine* e, int flags, double* out_device);
+int pg_check_errors(pg_engine* e);
+
+/* Run on a caller-provided cudaStream_t (e.g. torch's current stream). */
+int pg_set_stream(pg_engine* e, void* cuda_stream);
+
+/* engine.hpp:134-141 debug accessors (needs capture_partials): m x P
+ * column-major partials of one (node, category) and the per-pattern log
+ * scalers; values are scaled: true partial = partial * exp(scaler). */
+int pg_get_partials(pg_engine* e, int node, int category, double* post, double* pre, double* post_scaler,
+                    double* pre_scaler);
+/* Per-pattern site log-likelihoods of the last evaluation (P doubles). */
+int pg_get_site_log_likelihoods(pg_engine* e, double* out);
+
+/* engine.hpp:126-130 instrumentation. */
+uint64_t pg_node_visits(const pg_engine* e);
+void pg_reset_node_visits(pg_engine* e);
+void pg_invalidate_caches(pg_engine* e);
+
+/* Introspection for benchmarks: kernels launched by the last evaluation,
+ * average device ms of the walk kernel over the last evaluation, the chosen
+ * launch geometry. */
+int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states);
+int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms);
+
+/* ---- setup-side formats either side of the path ---- */
+/* tree.hpp:144-289 parse_newick: two calls — first with arrays NULL to learn
+ * tip_count, then with parent[2N], children[2N*2], branch_length[2N] (index =
+ * node, [root] = 0), post_order[2N-1]; labels written NUL-separated into
+ * label_buf (tips 1..N). */
+int pg_newick_parse(const char* text, int* tip_count, int32_t* parent, int32_t* children, double* branch_length,
+                    int32_t* post_order, char* label_buf, int64_t label_cap);
+
+/* alignment.hpp:186-229 from_codes compression, first-occurrence order.
+ * codes [ntax][sites] int32 in -1..m-1 (validated).  Returns a handle and the
+ * pattern count; pg_compress_result then writes pattern_codes [ntax][P]
+ * (int32), weights[P] and, if non-NULL, site_to_pattern[sites].  Hashing is
+ * multithreaded; the output order is bit-exact with the reference's std::map
+ * first-occurrence order. */
+int pg_compress_codes(int ntax, int64_t sites, const int32_t* codes, int state_count, void** handle,
+                      int* pattern_count);
+int pg_compress_result(void* handle, int32_t* pattern_codes, int64_t* weights, int32_t* site_to_pattern);
+void pg_compress_free(void* handle);
+
+/* Seeded synthetic workloads standing in for the paper's datasets
+ * (BASELINE.json configs): Yule tree, model draws, forward
+ * simulation, optional gaps, compression.  Host-side input generation only. */
+typedef struct pg_synth_spec {
+  int tips;
+  int model_kind;        /* 0 HKY85, 1 GTR, 2 general non-reversible 4-state, 3 AA-20 reversible, 4 GY94 codon */
+  int categories;        /* 1 or discrete-gamma count */
+  double gamma_alpha;
+  int64_t sites;
+  double branch_mean;    /* Exp(mean) branch lengths (model_kind != clock) */
+  int clock;             /* 1: b_i = r_i dt_i with dt ~ Exp(dt_mean), r = rate_scale*exp(N(0, rate_sd^2)) */
+  double dt_mean, rate_scale, rate_sd;
+  double gap_fraction;   /* Bernoulli per (taxon, site) -> missing */
+  uint64_t seed;
+  int threads;           /* 0 = hardware concurrency */
+} pg_synth_spec;
+int pg_synth_create(const pg_synth_spec* spec, void** handle, int* pattern_count, int* state_count);
+/* parent[2N], children[2N*2], post_order[2N-1], branch_lengths[2N-2],
+ * durations[2N-2] (zeros unless clock), rates[2N-2] (zeros unless clock). */
+int pg_synth_tree(void* handle, int32_t* parent, int32_t* children, int32_t* post_order, double* branch_lengths,
+                  double* durations, double* rates);
+int pg_synth_model(void* handle, double* q, double* pi, int* reversible, double* cat_rates, double* cat_probs);
+/* codes [tips][P] int8 (-1 missing), weights[P]. */
+int pg_synth_patterns(void* handle, int8_t* codes, int64_t* weights);
+void pg_synth_free(void* handle);
+
+/* substitution.hpp:55-68 discrete_gamma_categories (bin medians, mean one). */
+int pg_discrete_gamma(double alpha, int count, double* rates, double* probs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHYLOGRAD_B200_H */

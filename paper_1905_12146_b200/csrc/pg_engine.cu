@@ -1,0 +1,854 @@
+// phylograd-b200 engine: host orchestration of the sm_100a kernels behind the
+// C-ABI in include/phylograd_b200.h.  Mirrors phylograd::LikelihoodEngine
+// (/root/reference/proj/include/phylograd/engine.hpp:47-438): same setup
+// contract, cache semantics (engine.hpp:116-130, :146-162), node-visit
+// instrumentation and error messages; the arithmetic runs on the GPU only.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pg_common.hpp"
+#include "pg_kernels.cuh"
+#include "pg_walk.cuh"
+
+void* pg_walk_kernel_small(int MP, int LC);
+void* pg_walk_kernel_mid(int MP, int LC);
+void* pg_walk_kernel_large(int MP, int LC);
+
+namespace pg {
+namespace {
+
+#define PG_CUDA(call)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess) throw CudaError(std::string("cuda: ") + #call + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    release();
+    PG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count) PG_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+}  // namespace pg
+
+using namespace pg;
+
+struct pg_engine {
+  pg_options opt{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+
+  // topology (reference numbering)
+  int N = 0;
+  std::vector<int> parent, children;  // [2N], [2N*2]
+  std::vector<int4> post_steps, pre_steps;
+  // patterns
+  int m_aln = 0, P = 0, A = 0;
+  bool has_patterns = false;
+  std::vector<double> amb;  // [A][m]
+  // model
+  int m = 0;
+  bool has_model = false, reversible = false, have_eigen = false;
+  std::vector<double> q, pi, eig_u, eig_ui, eig_w;
+  std::map<int, std::vector<double>> branch_q;
+  // categories
+  int L = 0;
+  std::vector<double> rates, probs;
+  // lengths
+  std::vector<double> blen, dt;
+  bool has_dt = false;
+
+  // geometry
+  int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
+  bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
+
+  // device state
+  DevBuf<uint8_t> d_codes;
+  DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
+  DevBuf<int> d_qidx, d_err;
+  DevBuf<int4> d_post, d_pre;
+  DevBuf<double> d_escr, d_qscr, d_acc, d_out, d_site_ll;
+  DevBuf<double> d_cap_post, d_cap_pre;
+  DevBuf<int> d_cap_post_exp, d_cap_pre_exp;
+  double* h_out = nullptr;  // pinned
+  int* h_err = nullptr;     // pinned [3]
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+
+  // caches (engine.hpp:436)
+  bool post_valid = false, pre_valid = false, hess_valid = false, ll_valid = false, rate_grad = false;
+  double logl = 0.0;
+  std::vector<double> grad, hess;
+  uint64_t visits = 0;
+  int last_launches = 0;
+  float last_walk_ms = 0.f, last_total_ms = 0.f;
+  int pending_flags = 0;
+
+  ~pg_engine() {
+    if (h_out) cudaFreeHost(h_out);
+    if (h_err) cudaFreeHost(h_err);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  int B() const { return 2 * N - 2; }
+  void invalidate() { post_valid = pre_valid = hess_valid = ll_valid = false; }
+
+  void set_device() { PG_CUDA(cudaSetDevice(device)); }
+
+  // ---------------------------------------------------------------- setup
+  void set_topology(int nt, const int32_t* par, const int32_t* ch, const int32_t* post) {
+    if (nt < 2) throw std::invalid_argument("tree needs at least 2 tips");
+    const int n = 2 * nt - 1;
+    std::vector<int> pa(par, par + n + 1), cc(ch, ch + 2 * (n + 1));
+    // tree.hpp:81-126 validate_tree (structural part)
+    if (pa[size_t(n)] != 0) throw std::invalid_argument("root must have no parent");
+    for (int i = 1; i < n; ++i) {
+      const int p = pa[size_t(i)];
+      if (p <= nt || p > n) throw std::invalid_argument("node " + std::to_string(i) + " has invalid parent");
+      if (cc[size_t(2 * p)] != i && cc[size_t(2 * p + 1)] != i)
+        throw std::invalid_argument("parent/children maps inconsistent at node " + std::to_string(i));
+    }
+    for (int i = nt + 1; i <= n; ++i)
+      for (int k = 0; k < 2; ++k) {
+        const int c = cc[size_t(2 * i + k)];
+        if (c < 1 || c >= n || pa[size_t(c)] != i)
+          throw std::invalid_argument("bad child link at internal node " + std::to_string(i));
+      }
+    for (int i = 1; i <= nt; ++i)
+      if (cc[size_t(2 * i)] != 0 || cc[size_t(2 * i + 1)] != 0)
+        throw std::invalid_argument("bad child link at tip " + std::to_string(i));
+    for (int i = 1; i < n; ++i) {
+      int hops = 0, v = i;
+      while (v != n && hops++ <= n) v = pa[size_t(v)];
+      if (hops > n) throw std::invalid_argument("parent links contain a cycle");
+    }
+    if (post) {
+      std::vector<int> pos(size_t(n + 1), -1);
+      for (int k = 0; k < n; ++k) {
+        const int v = post[k];
+        if (v < 1 || v > n || pos[size_t(v)] >= 0) throw std::invalid_argument("post_order incomplete");
+        pos[size_t(v)] = k;
+      }
+      for (int i = 1; i < n; ++i)
+        if (pos[size_t(i)] >= pos[size_t(pa[size_t(i)])])
+          throw std::invalid_argument("post_order does not visit children before parents");
+    }
+    N = nt;
+    parent = pa;
+    children = cc;
+    build_schedule();
+    blen.assign(size_t(B()), 0.0);
+    dt.clear();
+    has_dt = false;
+    geometry_dirty = model_dirty = tc_dirty = true;
+    invalidate();
+  }
+
+  // Heavy-child-first post order over internal nodes (Sethi-Ullman-like): the
+  // arithmetic at each node is order independent, so this only changes which
+  // edge messages are still on chip when their parent needs them.
+  void build_schedule() {
+    const int n = 2 * N - 1;
+    std::vector<int> size(size_t(n + 1), 1);
+    // children have smaller completion index only in the reference numbering's
+    // internal block; compute sizes by explicit post traversal.
+    std::vector<int> order;
+    order.reserve(size_t(n));
+    std::vector<std::pair<int, bool>> st{{n, false}};
+    while (!st.empty()) {
+      auto [v, ex] = st.back();
+      st.pop_back();
+      if (v <= N || ex) {
+        order.push_back(v);
+      } else {
+        st.push_back({v, true});
+        st.push_back({children[size_t(2 * v + 1)], false});
+        st.push_back({children[size_t(2 * v)], false});
+      }
+    }
+    for (int v : order)
+      if (v > N) size[size_t(v)] = size[size_t(children[size_t(2 * v)])] + size[size_t(children[size_t(2 * v + 1)])];
+    post_steps.clear();
+    st.push_back({n, false});
+    while (!st.empty()) {
+      auto [v, ex] = st.back();
+      st.pop_back();
+      if (v <= N) continue;
+      const int c0 = children[size_t(2 * v)], c1 = children[size_t(2 * v + 1)];
+      if (ex) {
+        post_steps.push_back(make_int4(v, c0, c1, 0));
+        continue;
+      }
+      st.push_back({v, true});
+      const bool c0_heavy = size[size_t(c0)] >= size[size_t(c1)];
+      const int heavy = c0_heavy ? c0 : c1, light = c0_heavy ? c1 : c0;
+      st.push_back({light, false});
+      st.push_back({heavy, false});  // popped first
+    }
+    pre_steps.assign(post_steps.rbegin(), post_steps.rend());
+    for (size_t i = 0; i < pre_steps.size(); ++i) {
+      int next = 0;
+      if (i + 1 < pre_steps.size()) {
+        const int nx = pre_steps[i + 1].x;
+        if (parent[size_t(nx)] == pre_steps[i].x) next = nx;
+      }
+      pre_steps[i].w = next;
+    }
+  }
+
+  void set_patterns(int mm, int np, const int8_t* codes, int na, const double* ambig, const int64_t* w) {
+    if (N == 0) throw std::logic_error("engine: set the topology before the patterns");
+    if (mm < 2) throw std::invalid_argument("alignment: state count must be >= 2");
+    if (mm > 64) throw NotSupported("engine: at most 64 states are supported");
+    if (np < 0) throw std::invalid_argument("alignment: negative pattern count");
+    if (mm + na + 1 > 127) throw std::invalid_argument("alignment: too many ambiguity classes");
+    // MP depends on m; column index encoding: state s -> s, class a -> MP + a,
+    // missing -> MP + na (an extra all-ones class, alignment.hpp:223-224).
+    const int mp = mm <= 4 ? 4 : mm <= 8 ? 8 : mm <= 20 ? 20 : mm <= 32 ? 32 : 64;
+    std::vector<uint8_t> col(size_t(N) * size_t(np));
+    bool any_missing = false;
+    for (size_t i = 0; i < col.size(); ++i) {
+      const int c = codes[i];
+      if (c < -1 || c >= mm + na) throw std::invalid_argument("alignment: state code out of range");
+      if (c == -1) any_missing = true;
+      col[i] = uint8_t(c < 0 ? mp + na : c < mm ? c : mp + (c - mm));
+    }
+    std::vector<double> ambv(size_t(na + 1) * mm, 1.0);
+    for (int a = 0; a < na; ++a)
+      for (int j = 0; j < mm; ++j) ambv[size_t(a) * mm + j] = ambig[size_t(a) * mm + j];
+    (void)any_missing;
+    std::vector<double> wd(static_cast<size_t>(np));
+    for (int s = 0; s < np; ++s) {
+      if (w[s] < 0) throw std::invalid_argument("alignment: negative pattern weight");
+      wd[size_t(s)] = double(w[s]);
+    }
+    set_device();
+    d_codes.upload(col.data(), col.size(), stream);
+    d_weights.upload(wd.data(), wd.size(), stream);
+    d_amb.upload(ambv.data(), ambv.size(), stream);
+    PG_CUDA(cudaStreamSynchronize(stream));
+    m_aln = mm;
+    P = np;
+    A = na + 1;
+    amb = ambv;
+    has_patterns = true;
+    geometry_dirty = tc_dirty = true;
+    invalidate();
+  }
+
+  static void check_generator(const double* g, int mm) {
+    for (int i = 0; i < mm * mm; ++i)
+      if (!std::isfinite(g[i])) throw std::invalid_argument("generator: non-finite entries");
+    for (int i = 0; i < mm; ++i) {
+      double row = 0.0;
+      for (int j = 0; j < mm; ++j) {
+        if (i != j && g[i * mm + j] < 0.0) throw std::invalid_argument("generator: negative off-diagonal entry");
+        row += g[i * mm + j];
+      }
+      if (std::fabs(row) > 1e-12) throw std::invalid_argument("generator: rows must sum to zero");
+    }
+  }
+
+  void set_model(int mm, const double* qq, const double* pp, int rev) {
+    if (mm < 2 || mm > 64) throw std::invalid_argument("model: state count must be in 2..64");
+    check_generator(qq, mm);
+    double s = 0;
+    for (int i = 0; i < mm; ++i) {
+      if (pp[i] < -1e-12) throw std::invalid_argument("model: pi must be a probability vector");
+      s += pp[i];
+    }
+    if (std::fabs(s - 1.0) > 1e-12) throw std::invalid_argument("model: pi must be a probability vector");
+    m = mm;
+    q.assign(qq, qq + mm * mm);
+    pi.assign(pp, pp + mm);
+    reversible = rev != 0;
+    branch_q.clear();
+    // substitution.hpp:196-208: symmetric similarity transform
+    have_eigen = false;
+    bool positive = true;
+    for (double v : pi) positive = positive && v > 0.0;
+    if (reversible && positive) {
+      std::vector<double> sp(static_cast<size_t>(mm)), sym(static_cast<size_t>(mm) * mm);
+      for (int i = 0; i < mm; ++i) sp[size_t(i)] = std::sqrt(pi[size_t(i)]);
+      for (int i = 0; i < mm; ++i)
+        for (int j = 0; j < mm; ++j) {
+          const double a = sp[size_t(i)] * q[size_t(i) * mm + j] / sp[size_t(j)];
+          const double b = sp[size_t(j)] * q[size_t(j) * mm + i] / sp[size_t(i)];
+          sym[size_t(i) * mm + j] = 0.5 * (a + b);
+        }
+      std::vector<double> V;
+      symmetric_eigen(sym, mm, eig_w, V);
+      eig_u.assign(size_t(mm) * mm, 0.0);
+      eig_ui.assign(size_t(mm) * mm, 0.0);
+      for (int i = 0; i < mm; ++i)
+        for (int j = 0; j < mm; ++j) {
+          eig_u[size_t(i) * mm + j] = V[size_t(i) * mm + j] / sp[size_t(i)];
+          eig_ui[size_t(i) * mm + j] = V[size_t(j) * mm + i] * sp[size_t(j)];
+        }
+      have_eigen = true;
+    }
+    has_model = true;
+    model_dirty = tc_dirty = geometry_dirty = true;
+    invalidate();
+  }
+
+  void set_branch_generator(int branch, const double* qq) {
+    if (!has_model) throw std::logic_error("engine: set the model before branch generators");
+    if (branch < 1 || branch > B()) throw std::invalid_argument("branch generator: branch out of range");
+    check_generator(qq, m);
+    branch_q[branch] = std::vector<double>(qq, qq + m * m);
+    model_dirty = tc_dirty = true;
+    invalidate();
+  }
+
+  void set_categories(int nl, const double* r, const double* pr) {
+    if (nl < 1) throw std::invalid_argument("rate categories: need L >= 1 matched rates/probs");
+    double ps = 0, mean = 0;
+    for (int l = 0; l < nl; ++l) {
+      if (!(r[l] > 0.0)) throw std::invalid_argument("rate categories: rates must be positive");
+      ps += pr[l];
+      mean += r[l] * pr[l];
+    }
+    if (std::fabs(ps - 1.0) > 1e-12) throw std::invalid_argument("rate categories: probabilities must sum to 1");
+    if (std::fabs(mean - 1.0) > 1e-10) throw std::invalid_argument("rate categories: mixture mean must be 1");
+    if (nl > 128) throw NotSupported("engine: at most 128 rate categories");
+    L = nl;
+    rates.assign(r, r + nl);
+    probs.assign(pr, pr + nl);
+    set_device();
+    d_rates.upload(rates.data(), size_t(L), stream);
+    d_probs.upload(probs.data(), size_t(L), stream);
+    PG_CUDA(cudaStreamSynchronize(stream));
+    geometry_dirty = tc_dirty = true;
+    invalidate();
+  }
+
+  void set_branch_lengths(const double* b) {
+    if (N == 0) throw std::logic_error("engine: set the topology first");
+    bool same = true;
+    for (int i = 0; i < B(); ++i) {
+      if (!std::isfinite(b[i]) || b[i] < 0.0)
+        throw std::invalid_argument("engine: branch lengths must be finite and nonnegative");
+      if (b[i] != blen[size_t(i)]) same = false;
+    }
+    if (same && !tc_dirty) return;  // caches stay valid (engine.hpp:121)
+    std::copy(b, b + B(), blen.begin());
+    set_device();
+    d_blen.upload(blen.data(), blen.size(), stream);
+    tc_dirty = true;
+    invalidate();
+  }
+
+  void set_branch_lengths_device(const double* b) {
+    if (N == 0) throw std::logic_error("engine: set the topology first");
+    set_device();
+    d_blen.ensure(size_t(B()));
+    PG_CUDA(cudaMemcpyAsync(d_blen.p, b, sizeof(double) * size_t(B()), cudaMemcpyDeviceToDevice, stream));
+    PG_CUDA(cudaMemcpyAsync(blen.data(), b, sizeof(double) * size_t(B()), cudaMemcpyDeviceToHost, stream));
+    tc_dirty = true;
+    invalidate();
+  }
+
+  void set_durations(const double* d) {
+    if (N == 0) throw std::logic_error("engine: set the topology first");
+    for (int i = 0; i < B(); ++i)
+      if (!std::isfinite(d[i]) || d[i] < 0.0) throw std::invalid_argument("clock: durations must be finite and nonnegative");
+    dt.assign(d, d + B());
+    has_dt = true;
+    set_device();
+    d_dt.upload(dt.data(), dt.size(), stream);
+    PG_CUDA(cudaStreamSynchronize(stream));
+    invalidate();
+  }
+
+  // ------------------------------------------------------------ prepare
+  void check_ready() {
+    if (N == 0) throw std::logic_error("engine: topology not set");
+    if (!has_patterns) throw std::logic_error("engine: patterns not set");
+    if (!has_model) throw std::logic_error("engine: model not set");
+    if (L == 0) throw std::logic_error("engine: rate categories not set");
+    if (m_aln != m) throw std::invalid_argument("engine: alignment/model state counts differ");
+  }
+
+  void upload_model() {
+    std::vector<double> qt(size_t(1 + branch_q.size()) * MP * MP, 0.0), pipad(size_t(MP), 0.0);
+    std::vector<int> qidx(size_t(2 * N), 0);
+    auto put = [&](int slot, const std::vector<double>& g) {
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) qt[size_t(slot) * MP * MP + size_t(i) * MP + j] = g[size_t(i) * m + j];
+    };
+    put(0, q);
+    int slot = 1;
+    for (auto& [br, g] : branch_q) {
+      put(slot, g);
+      qidx[size_t(br)] = slot++;
+    }
+    for (int i = 0; i < m; ++i) pipad[size_t(i)] = pi[size_t(i)];
+    d_qtab.upload(qt.data(), qt.size(), stream);
+    d_qidx.upload(qidx.data(), qidx.size(), stream);
+    d_pi.upload(pipad.data(), pipad.size(), stream);
+    if (have_eigen) {
+      d_eu.upload(eig_u.data(), eig_u.size(), stream);
+      d_eui.upload(eig_ui.data(), eig_ui.size(), stream);
+      d_ew.upload(eig_w.data(), eig_w.size(), stream);
+    } else {
+      d_eu.ensure(1);
+      d_eui.ensure(1);
+      d_ew.ensure(1);
+    }
+    model_dirty = false;
+  }
+
+  int walk_max_blocks_per_sm();
+
+  void prepare_geometry() {
+    MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
+    NC = MP + A;
+    const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;
+    LC = std::min(maxLC, pow2ceil(L));
+    // Prefer more, smaller tiles when the pattern count cannot fill the GPU.
+    while (LC > 1 && (int64_t(P) * pow2ceil((L + LC - 1) / LC)) / 32 < int64_t(num_sms) * 8) LC >>= 1;
+    G = pow2ceil((L + LC - 1) / LC);
+    if (G > 32) throw NotSupported("engine: too many rate categories for the lane layout");
+    const int TP = 32 / G;
+    ntiles = (P + TP - 1) / TP;
+    const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
+    const size_t vec = size_t(32) * LC * MP;
+    const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
+    size_t free_b = 0, total_b = 0;
+    PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = size_t(double(free_b) * 0.6);
+    int cap = int(std::max<size_t>(1, budget / per_warp));
+    TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
+    TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
+    accw = 1 + 2 * B();
+    d_escr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
+    d_qscr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
+    d_acc.ensure(size_t(TW) * size_t(accw));
+    d_out.ensure(size_t(accw));
+    d_site_ll.ensure(size_t(std::max(P, 1)));
+    d_err.ensure(3);
+    d_tc.ensure(size_t(B()) * L * NC * MP);
+    d_post.upload(post_steps.data(), post_steps.size(), stream);
+    d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
+    if (!h_out) {
+      PG_CUDA(cudaMallocHost(&h_err, 3 * sizeof(int)));
+      PG_CUDA(cudaEventCreate(&ev0));
+      PG_CUDA(cudaEventCreate(&ev1));
+      PG_CUDA(cudaEventCreate(&ev2));
+    }
+    if (h_out) cudaFreeHost(h_out);
+    PG_CUDA(cudaMallocHost(&h_out, size_t(accw) * sizeof(double)));
+    if (opt.capture_partials) {
+      const size_t nn = size_t(2 * N);
+      d_cap_post.ensure(nn * L * size_t(P) * MP);
+      d_cap_pre.ensure(nn * L * size_t(P) * MP);
+      d_cap_post_exp.ensure(nn * size_t(P));
+      d_cap_pre_exp.ensure(nn * size_t(P));
+      PG_CUDA(cudaMemsetAsync(d_cap_post.p, 0, d_cap_post.n * sizeof(double), stream));
+      PG_CUDA(cudaMemsetAsync(d_cap_pre.p, 0, d_cap_pre.n * sizeof(double), stream));
+      PG_CUDA(cudaMemsetAsync(d_cap_post_exp.p, 0, d_cap_post_exp.n * sizeof(int), stream));
+      PG_CUDA(cudaMemsetAsync(d_cap_pre_exp.p, 0, d_cap_pre_exp.n * sizeof(int), stream));
+    }
+    if (d_blen.n < size_t(B())) d_blen.upload(blen.data(), blen.size(), stream);
+    geometry_dirty = false;
+    model_dirty = true;
+  }
+
+  void launch_tc();
+  void launch_walk(bool do_pre, bool do_hess);
+
+  // ------------------------------------------------------------ evaluate
+  // Enqueues the evaluation; results land in d_out (or out_device).
+  void enqueue(int flags, double* out_device) {
+    check_ready();
+    set_device();
+    if (geometry_dirty) prepare_geometry();
+    if (model_dirty) upload_model();
+    const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
+    const bool want_hess = flags & PG_EVAL_HESS;
+    if ((flags & PG_EVAL_RATE_GRAD) && !has_dt) throw std::logic_error("engine: rate gradient needs clock durations");
+    int launches = 0;
+    PG_CUDA(cudaMemsetAsync(d_err.p, 0x7f, 3 * sizeof(int), stream));  // INT_MAX-ish sentinel
+    PG_CUDA(cudaEventRecord(ev0, stream));
+    if (tc_dirty) {
+      launch_tc();
+      ++launches;
+      tc_dirty = false;
+    }
+    PG_CUDA(cudaEventRecord(ev1, stream));
+    launch_walk(want_grad, want_hess);
+    ++launches;
+    PG_CUDA(cudaEventRecord(ev2, stream));
+    const int width = want_hess ? accw : 1 + B();
+    double* out = out_device ? out_device : d_out.p;
+    pgk::reduce_kernel<<<(width + 255) / 256, 256, 0, stream>>>(
+        d_acc.p, TW, accw, width, out, (flags & PG_EVAL_RATE_GRAD) ? d_dt.p : nullptr, B());
+    PG_CUDA(cudaGetLastError());
+    ++launches;
+    last_launches = launches;
+    PG_CUDA(cudaMemcpyAsync(h_err, d_err.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    pending_flags = flags;
+  }
+
+  void check_errors() {
+    PG_CUDA(cudaStreamSynchronize(stream));
+    PG_CUDA(cudaEventElapsedTime(&last_walk_ms, ev1, ev2));
+    PG_CUDA(cudaEventElapsedTime(&last_total_ms, ev0, ev2));
+    if (h_err[2] == 1) throw std::invalid_argument("transition matrix: negative branch length");
+    const int nf = h_err[0], uf = h_err[1];
+    const int sentinel = 0x7f7f7f7f;
+    if (nf != sentinel || uf != sentinel) {
+      if (nf <= uf) throw std::runtime_error("engine: non-finite partial at pattern " + std::to_string(nf));
+      throw std::runtime_error("engine: site likelihood underflowed to zero at pattern " + std::to_string(uf));
+    }
+  }
+
+  void evaluate(int flags, double* ll_out, double* g_out, double* h_out_) {
+    if ((flags & PG_EVAL_REQUIRE_POST) && !post_valid)
+      throw std::logic_error("engine: pre-order pass requires a current post-order pass");
+    if (flags & PG_EVAL_FORCE) invalidate();
+    const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
+    const bool want_hess = flags & PG_EVAL_HESS;
+    const bool rate = flags & PG_EVAL_RATE_GRAD;
+    const bool post_pass = flags & PG_EVAL_POST_PASS;
+    const bool cached = want_grad ? (pre_valid && post_valid && (!want_hess || hess_valid) && rate == rate_grad)
+                                  : (post_pass ? post_valid : ll_valid);
+    if (!cached) {
+      enqueue(flags, nullptr);
+      const int width = want_hess ? accw : (want_grad ? 1 + B() : 1);
+      PG_CUDA(cudaMemcpyAsync(h_out, d_out.p, size_t(width) * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      try {
+        check_errors();
+      } catch (...) {
+        invalidate();
+        throw;
+      }
+      logl = h_out[0];
+      ll_valid = true;
+      if (want_grad) {
+        // reference: post visits only when the post cache was stale
+        visits += uint64_t(post_valid ? 0 : 2 * N - 1) + uint64_t(2 * N - 1);
+        grad.assign(h_out + 1, h_out + 1 + B());
+        if (want_hess) hess.assign(h_out + 1 + B(), h_out + 1 + 2 * B());
+        post_valid = pre_valid = true;
+        hess_valid = want_hess;
+        rate_grad = rate;
+      } else if (post_pass) {
+        visits += uint64_t(2 * N - 1);  // post_order_pass (engine.hpp:188)
+        post_valid = true;
+        pre_valid = hess_valid = false;
+      } else {
+        visits += uint64_t(2 * N - 1);  // scratch likelihood route (engine.hpp:308-309)
+      }
+    }
+    if (ll_out) *ll_out = logl;
+    if (want_grad && g_out) std::copy(grad.begin(), grad.end(), g_out);
+    if (want_hess && h_out_) std::copy(hess.begin(), hess.end(), h_out_);
+  }
+};
+
+namespace {
+
+void* select_walk(int MP, int LC) {
+  void* f = pg_walk_kernel_small(MP, LC);
+  if (!f) f = pg_walk_kernel_mid(MP, LC);
+  if (!f) f = pg_walk_kernel_large(MP, LC);
+  if (!f) throw NotSupported("engine: no kernel for this state/category layout");
+  return f;
+}
+
+}  // namespace
+
+int pg_engine::walk_max_blocks_per_sm() {
+  const int mp = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
+  const int maxLC = mp == 4 ? 4 : mp == 8 ? 2 : 1;
+  int nb = 0;
+  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_walk(mp, std::min(maxLC, pow2ceil(L))),
+                                                        pgk::kWarpsPerBlock * 32, 0));
+  return std::max(nb, 1);
+}
+
+void pg_engine::launch_tc() {
+  pgk::TcParams p{};
+  p.blen = d_blen.p;
+  p.rates = d_rates.p;
+  p.qtab = d_qtab.p;
+  p.qidx = d_qidx.p;
+  p.eig_u = d_eu.p;
+  p.eig_ui = d_eui.p;
+  p.eig_w = d_ew.p;
+  p.amb = d_amb.p;
+  p.tc = d_tc.p;
+  p.err = d_err.p;
+  p.m = m;
+  p.MP = MP;
+  p.NC = NC;
+  p.A = A;
+  p.L = L;
+  p.have_eigen = have_eigen ? 1 : 0;
+  const size_t smem = (size_t(7) * m * m + m) * sizeof(double);
+  if (smem > 48 * 1024)
+    PG_CUDA(cudaFuncSetAttribute(pgk::tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid{unsigned(B()), unsigned(L), 1u};
+  pgk::tc_kernel<<<grid, 128, smem, stream>>>(p);
+  PG_CUDA(cudaGetLastError());
+}
+
+void pg_engine::launch_walk(bool do_pre, bool do_hess) {
+  pgk::WalkParams p{};
+  p.codes = d_codes.p;
+  p.weights = d_weights.p;
+  p.tc = d_tc.p;
+  p.qtab = d_qtab.p;
+  p.qidx = d_qidx.p;
+  p.pi = d_pi.p;
+  p.rates = d_rates.p;
+  p.probs = d_probs.p;
+  p.post = d_post.p;
+  p.pre = d_pre.p;
+  p.escr = d_escr.p;
+  p.qscr = d_qscr.p;
+  p.acc = d_acc.p;
+  p.err = d_err.p;
+  p.site_ll = d_site_ll.p;
+  if (opt.capture_partials) {
+    p.cap_post = d_cap_post.p;
+    p.cap_pre = d_cap_pre.p;
+    p.cap_post_exp = d_cap_post_exp.p;
+    p.cap_pre_exp = d_cap_pre_exp.p;
+  }
+  p.N = N;
+  p.P = P;
+  p.L = L;
+  p.G = G;
+  p.NC = NC;
+  p.nsteps = int(post_steps.size());
+  p.ntiles = ntiles;
+  p.accw = accw;
+  p.B = B();
+  p.thr = opt.rescaling_threshold;
+  p.force = opt.force_rescaling;
+  p.disable = opt.disable_rescaling;
+  p.do_pre = do_pre ? 1 : 0;
+  p.hess = do_hess ? 1 : 0;
+  void* fn = select_walk(MP, LC);
+  void* args[] = {&p};
+  PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args, 0,
+                           stream));
+}
+
+// ============================================================== C-ABI
+extern "C" {
+
+void pg_default_options(pg_options* opt) {
+  std::memset(opt, 0, sizeof(*opt));
+  opt->rescaling_threshold = 1e-150;
+}
+
+int pg_create(const pg_options* opt, pg_engine** out) {
+  return guarded([&] {
+    auto e = std::make_unique<pg_engine>();
+    if (opt) e->opt = *opt;
+    else pg_default_options(&e->opt);
+    e->device = e->opt.device;
+    int count = 0;
+    PG_CUDA(cudaGetDeviceCount(&count));
+    if (e->device < 0 || e->device >= count) throw CudaError("engine: CUDA device not available");
+    e->set_device();
+    PG_CUDA(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
+    PG_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->own_stream = true;
+    *out = e.release();
+  });
+}
+
+void pg_destroy(pg_engine* e) { delete e; }
+
+int pg_set_topology(pg_engine* e, int tip_count, const int32_t* parent, const int32_t* children,
+                    const int32_t* post_order) {
+  return guarded([&] { e->set_topology(tip_count, parent, children, post_order); });
+}
+
+int pg_set_patterns(pg_engine* e, int state_count, int pattern_count, const int8_t* codes, int ambiguity_count,
+                    const double* ambiguity, const int64_t* weights) {
+  return guarded([&] { e->set_patterns(state_count, pattern_count, codes, ambiguity_count, ambiguity, weights); });
+}
+
+int pg_set_model(pg_engine* e, int state_count, const double* q, const double* pi, int reversible) {
+  return guarded([&] { e->set_model(state_count, q, pi, reversible); });
+}
+
+int pg_set_branch_generator(pg_engine* e, int branch, const double* q) {
+  return guarded([&] { e->set_branch_generator(branch, q); });
+}
+
+int pg_set_categories(pg_engine* e, int category_count, const double* rates, const double* probs) {
+  return guarded([&] { e->set_categories(category_count, rates, probs); });
+}
+
+int pg_set_branch_lengths(pg_engine* e, const double* b) {
+  return guarded([&] { e->set_branch_lengths(b); });
+}
+
+int pg_set_branch_lengths_device(pg_engine* e, const double* b_device) {
+  return guarded([&] { e->set_branch_lengths_device(b_device); });
+}
+
+int pg_get_branch_lengths(const pg_engine* e, double* b) {
+  return guarded([&] { std::copy(e->blen.begin(), e->blen.end(), b); });
+}
+
+int pg_set_clock_durations(pg_engine* e, const double* dt) {
+  return guarded([&] { e->set_durations(dt); });
+}
+
+int pg_evaluate(pg_engine* e, int flags, double* log_likelihood, double* grad, double* hess) {
+  return guarded([&] {
+    if ((flags & (PG_EVAL_GRAD | PG_EVAL_RATE_GRAD)) && !grad && (flags & PG_EVAL_GRAD))
+      throw std::invalid_argument("pg_evaluate: gradient requested without an output buffer");
+    e->evaluate(flags, log_likelihood, grad, hess);
+  });
+}
+
+int pg_evaluate_device(pg_engine* e, int flags, double* out_device) {
+  return guarded([&] {
+    if (!out_device) throw std::invalid_argument("pg_evaluate_device: null output");
+    e->invalidate();
+    e->enqueue(flags | PG_EVAL_FORCE, out_device);
+  });
+}
+
+int pg_check_errors(pg_engine* e) {
+  return guarded([&] {
+    const bool grad = e->pending_flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
+    e->check_errors();
+    e->visits += uint64_t(grad ? 2 : 1) * uint64_t(2 * e->N - 1);
+  });
+}
+
+int pg_set_stream(pg_engine* e, void* s) {
+  return guarded([&] {
+    if (e->own_stream && e->stream) {
+      PG_CUDA(cudaStreamSynchronize(e->stream));
+      PG_CUDA(cudaStreamDestroy(e->stream));
+    }
+    e->stream = static_cast<cudaStream_t>(s);
+    e->own_stream = false;
+  });
+}
+
+int pg_get_partials(pg_engine* e, int node, int category, double* post, double* pre, double* post_scaler,
+                    double* pre_scaler) {
+  return guarded([&] {
+    if (!e->opt.capture_partials) throw std::logic_error("engine: partial capture is disabled");
+    if (!e->pre_valid) throw std::logic_error("engine: no current gradient pass to read partials from");
+    const int n = 2 * e->N - 1;
+    if (node < 1 || node > n || category < 0 || category >= e->L)
+      throw std::invalid_argument("engine: node or category out of range");
+    e->set_device();
+    const int P = e->P, MP = e->MP, m = e->m;
+    const size_t nn = size_t(2 * e->N);
+    std::vector<double> cp(nn * e->L * size_t(P) * MP), cq(cp.size());
+    std::vector<int> ep(nn * size_t(P)), eq(ep.size());
+    PG_CUDA(cudaMemcpy(cp.data(), e->d_cap_post.p, cp.size() * 8, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(cq.data(), e->d_cap_pre.p, cq.size() * 8, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(ep.data(), e->d_cap_post_exp.p, ep.size() * 4, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(eq.data(), e->d_cap_pre_exp.p, eq.size() * 4, cudaMemcpyDeviceToHost));
+    // reconstruct per-node log scalers (engine.hpp:192, :252) from own exponents
+    std::vector<long> spost(nn * size_t(P), 0), spre(nn * size_t(P), 0);
+    // post: children before parents -> iterate the schedule
+    for (const int4& st : e->post_steps)
+      for (int s = 0; s < P; ++s)
+        spost[size_t(st.x) * P + s] =
+            spost[size_t(st.y) * P + s] + spost[size_t(st.z) * P + s] + ep[size_t(st.x) * P + s];
+    for (const int4& st : e->pre_steps)
+      for (int side = 0; side < 2; ++side) {
+        const int x = side ? st.z : st.y, y = side ? st.y : st.z;
+        for (int s = 0; s < P; ++s)
+          spre[size_t(x) * P + s] = spre[size_t(st.x) * P + s] + spost[size_t(y) * P + s] + eq[size_t(x) * P + s];
+      }
+    const double ln2 = 0.6931471805599453;
+    for (int s = 0; s < P; ++s) {
+      for (int j = 0; j < m; ++j) {
+        if (post) {
+          if (node <= e->N) post[size_t(s) * m + j] = std::numeric_limits<double>::quiet_NaN();  // tips: dense tip data lives on the host
+          else post[size_t(s) * m + j] = cp[((size_t(node) * e->L + category) * P + s) * MP + j];
+        }
+        if (pre) {
+          if (node == n) pre[size_t(s) * m + j] = e->pi[size_t(j)];
+          else pre[size_t(s) * m + j] = cq[((size_t(node) * e->L + category) * P + s) * MP + j];
+        }
+      }
+      if (post_scaler) post_scaler[s] = double(spost[size_t(node) * P + s]) * ln2;
+      if (pre_scaler) pre_scaler[s] = double(spre[size_t(node) * P + s]) * ln2;
+    }
+  });
+}
+
+int pg_get_site_log_likelihoods(pg_engine* e, double* out) {
+  return guarded([&] {
+    if (!e->ll_valid) throw std::logic_error("engine: no current evaluation");
+    e->set_device();
+    PG_CUDA(cudaMemcpy(out, e->d_site_ll.p, size_t(e->P) * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+uint64_t pg_node_visits(const pg_engine* e) { return e->visits; }
+void pg_reset_node_visits(pg_engine* e) { e->visits = 0; }
+void pg_invalidate_caches(pg_engine* e) { e->invalidate(); }
+
+int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states) {
+  return guarded([&] {
+    if (launches) *launches = e->last_launches;
+    if (total_warps) *total_warps = e->TW;
+    if (lanes_per_pattern) *lanes_per_pattern = e->G;
+    if (padded_states) *padded_states = e->MP;
+  });
+}
+
+int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {
+  return guarded([&] {
+    if (walk_ms) *walk_ms = e->last_walk_ms;
+    if (total_ms) *total_ms = e->last_total_ms;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// phylograd-b200 device code (sm_100a, fp64).
+//
+// Three kernel families replace LikelihoodEngine's hot loops
+// (/root/reference/proj/include/phylograd/engine.hpp):
+//
+//  K1 tc_kernel     — P(t) = e^{Q b c} per (branch, category) from the
+//                     symmetric eigensystem (substitution.hpp:147-160, :196-208)
+//                     or Pade scaling-and-squaring (substitution.hpp:71-75),
+//                     clamp >= 0, t == 0 -> I; stored as columns, followed by
+//                     P * (ambiguity partial) columns so every tip edge is a
+//                     gather (engine.hpp:367-382).
+//  K2 walk_kernel   — per-warp pattern tile walks the whole tree:
+//                     post-order pruning p_k = e_c0 o e_c1 with per-pattern
+//                     rescaling (engine.hpp:182-221, :396-414) and edge
+//                     messages e_k = P_k p_k, then the pre-order pass
+//                     q_c = P_c^T (q_k o e_sib) (engine.hpp:225-253) with the
+//                     gradient (and Hessian diagonal) fused in
+//                     (engine.hpp:255-274) using the self-normalised ratio
+//                     top^T Q e / top^T e (Eq. 8 node invariance).
+//  K3 reduce_kernel — fixed-order sum of the per-warp accumulators, then the
+//                     clock chain rule d/dr = dt * d/db (clock.hpp:146-152).
+#pragma once
+// K2 lives here; K1/K3 are in pg_kernels.cuh.
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pgk {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct WalkParams {
+  const uint8_t* codes;  // [N][P] tip column index into the TC table
+  const double* weights; // [P]
+  const double* tc;      // [B][L][NC][MP]: column c of P (c < MP) or P*ambiguity (c >= MP)
+  const double* qtab;    // [nq][MP][MP] row-major generators
+  const int* qidx;       // [2N] node -> generator index
+  const double* pi;      // [MP]
+  const double* rates;   // [L]
+  const double* probs;   // [L]
+  const int4* post;      // [nsteps] {k, c0, c1, 0} internal nodes, heavy-child-first post order
+  const int4* pre;       // [nsteps] {k, c0, c1, next} reverse of post; next = following step's node if a child of k
+  double* escr;          // [TW][N-1][VEC] edge messages e_k of internal non-root nodes
+  double* qscr;          // [TW][N-1][VEC] pre-order partials of deferred internal nodes
+  double* acc;           // [TW][accw]: [0] logL, [x] grad of branch x, [B+x] hess
+  int* err;              // [2] first non-finite pattern, first underflowed pattern
+  double* site_ll;       // [P] optional
+  double* cap_post;      // optional debug capture [(2N)][L][P][MP]
+  double* cap_pre;
+  int* cap_post_exp;     // [(2N)][P]
+  int* cap_pre_exp;
+  int N, P, L, G, NC, nsteps, ntiles, accw, B;
+  double thr;
+  int force, disable, do_pre, hess;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double group_sum(double v, int G) {
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double group_max(double v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// One lane holds LC categories x MP states of one pattern.  Slot layout is
+// [LC*MP/2][32 lanes] double2 so every warp access is 512 contiguous bytes.
+template <int MP, int LC>
+__device__ __forceinline__ void load_slot(const double* base, int lane, double (&v)[LC][MP]) {
+  const double2* src = reinterpret_cast<const double2*>(base);
+#pragma unroll
+  for (int q = 0; q < LC * MP / 2; ++q) {
+    const double2 d = __ldcg(src + q * 32 + lane);
+    v[(2 * q) / MP][(2 * q) % MP] = d.x;
+    v[(2 * q + 1) / MP][(2 * q + 1) % MP] = d.y;
+  }
+}
+template <int MP, int LC>
+__device__ __forceinline__ void store_slot(double* base, int lane, const double (&v)[LC][MP]) {
+  double2* dst = reinterpret_cast<double2*>(base);
+#pragma unroll
+  for (int q = 0; q < LC * MP / 2; ++q) {
+    double2 d;
+    d.x = v[(2 * q) / MP][(2 * q) % MP];
+    d.y = v[(2 * q + 1) / MP][(2 * q + 1) % MP];
+    __stcg(dst + q * 32 + lane, d);
+  }
+}
+
+// Tip edge message: gather column `code` of P (or of P * ambiguity partial).
+template <int MP, int LC>
+__device__ __forceinline__ void gather_tip(const WalkParams& p, int node, int sc, const int (&lc)[LC],
+                                           double (&v)[LC][MP]) {
+  const int col = p.codes[size_t(node - 1) * p.P + sc];
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    const double2* src =
+        reinterpret_cast<const double2*>(p.tc + ((size_t(node - 1) * p.L + lc[j]) * p.NC + col) * MP);
+#pragma unroll
+    for (int h = 0; h < MP / 2; ++h) {
+      const double2 d = __ldg(src + h);
+      v[j][2 * h] = d.x;
+      v[j][2 * h + 1] = d.y;
+    }
+  }
+}
+
+template <int MP, int LC>
+__device__ __forceinline__ int rescale(double (&v)[LC][MP], int G, double thr, int force, int disable) {
+  double pk = 0.0;
+#pragma unroll
+  for (int j = 0; j < LC; ++j)
+#pragma unroll
+    for (int i = 0; i < MP; ++i) pk = fmax(pk, v[j][i]);
+  pk = group_max(pk, G);
+  int ex = 0;
+  if (!disable && pk > 0.0 && (force || pk < thr)) {
+    frexp(pk, &ex);
+#pragma unroll
+    for (int j = 0; j < LC; ++j)
+#pragma unroll
+      for (int i = 0; i < MP; ++i) v[j][i] = ldexp(v[j][i], -ex);
+  }
+  return ex;
+}
+
+template <int MP, int LC>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_constant__ WalkParams p) {
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int TW = gridDim.x * kWarpsPerBlock;
+  const int G = p.G, TP = 32 / G;
+  const int g = lane & (G - 1), pl = lane / G;
+  const int root = 2 * p.N - 1;
+
+  int lc[LC];
+  double cw[LC], crw[LC], cr2w[LC];
+  bool creal[LC];
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    const int l = g * LC + j;
+    creal[j] = l < p.L;
+    lc[j] = creal[j] ? l : p.L - 1;
+    const double w = creal[j] ? p.probs[lc[j]] : 0.0, r = p.rates[lc[j]];
+    cw[j] = w;
+    crw[j] = r * w;
+    cr2w[j] = r * r * w;
+  }
+  constexpr size_t VEC = size_t(32) * LC * MP;
+  double* E = p.escr + size_t(warp) * size_t(p.N - 1) * VEC;
+  double* Qs = p.qscr + size_t(warp) * size_t(p.N - 1) * VEC;
+  double* A = p.acc + size_t(warp) * p.accw;
+  for (int i = lane; i < p.accw; i += 32) A[i] = 0.0;
+  __syncwarp();
+
+  for (int t = warp; t < p.ntiles; t += TW) {
+    const int s = t * TP + pl;
+    const bool valid = s < p.P;
+    const int sc = valid ? s : p.P - 1;
+    const double w = valid ? p.weights[sc] : 0.0;
+    const bool owner = valid && g == 0;
+
+    // ------------------------------------------------ post-order pass (a)
+    int S = 0;  // accumulated power-of-two rescale exponent of this pattern
+    double keep[LC][MP];
+    int last = -1;
+    for (int i = 0; i < p.nsteps; ++i) {
+      const int4 st = p.post[i];
+      const int k = st.x;
+      double x[LC][MP], y[LC][MP];
+      if (st.y <= p.N) gather_tip<MP, LC>(p, st.y, sc, lc, x);
+      else if (st.y == last) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+#pragma unroll
+          for (int q = 0; q < MP; ++q) x[j][q] = keep[j][q];
+      } else load_slot<MP, LC>(E + size_t(st.y - p.N - 1) * VEC, lane, x);
+      if (st.z <= p.N) gather_tip<MP, LC>(p, st.z, sc, lc, y);
+      else if (st.z == last) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+#pragma unroll
+          for (int q = 0; q < MP; ++q) y[j][q] = keep[j][q];
+      } else load_slot<MP, LC>(E + size_t(st.z - p.N - 1) * VEC, lane, y);
+
+#pragma unroll
+      for (int j = 0; j < LC; ++j)
+#pragma unroll
+        for (int q = 0; q < MP; ++q) x[j][q] *= y[j][q];
+      const int ex = rescale<MP, LC>(x, G, p.thr, p.force, p.disable);
+      S += ex;
+      if (p.cap_post && valid) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+          if (creal[j])
+            for (int q = 0; q < MP; ++q) p.cap_post[((size_t(k) * p.L + lc[j]) * p.P + s) * MP + q] = x[j][q];
+        if (g == 0) p.cap_post_exp[size_t(k) * p.P + s] = ex;
+      }
+      if (k == root) {
+        double mix = 0.0;
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          double d = 0.0;
+#pragma unroll
+          for (int q = 0; q < MP; ++q) d = fma(p.pi[q], x[j][q], d);
+          mix = fma(cw[j], d, mix);
+        }
+        mix = group_sum(mix, G);
+        const double ll = log(mix) + double(S) * 0.6931471805599453;
+        if (owner) {
+          if (!isfinite(mix)) atomicMin(&p.err[0], s);
+          else if (mix <= 0.0) atomicMin(&p.err[1], s);
+          if (p.site_ll) p.site_ll[s] = ll;
+        }
+        const double v = warp_sum(owner ? w * ll : 0.0);
+        if (lane == 0) A[0] += v;
+      } else {
+        // edge message e_k = P_k p_k (engine.hpp:367-372)
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          const double2* T =
+              reinterpret_cast<const double2*>(p.tc + (size_t(k - 1) * p.L + lc[j]) * p.NC * MP);
+          double e[MP];
+#pragma unroll
+          for (int q = 0; q < MP; ++q) e[q] = 0.0;
+#pragma unroll
+          for (int c = 0; c < MP; ++c) {
+            const double xc = x[j][c];
+#pragma unroll
+            for (int h = 0; h < MP / 2; ++h) {
+              const double2 col = __ldg(T + c * (MP / 2) + h);
+              e[2 * h] = fma(col.x, xc, e[2 * h]);
+              e[2 * h + 1] = fma(col.y, xc, e[2 * h + 1]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < MP; ++q) keep[j][q] = e[q];
+        }
+        store_slot<MP, LC>(E + size_t(k - p.N - 1) * VEC, lane, keep);
+        last = k;
+      }
+    }
+    if (!p.do_pre) continue;
+
+    // ----------------------------------- pre-order pass + gradient (b)+(c)
+    double qreg[LC][MP];
+    int qnode = -1;
+    for (int i = 0; i < p.nsteps; ++i) {
+      const int4 st = p.pre[i];
+      const int k = st.x;
+      double q[LC][MP];
+      if (k == root) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+#pragma unroll
+          for (int r = 0; r < MP; ++r) q[j][r] = p.pi[r];
+      } else if (k == qnode) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+#pragma unroll
+          for (int r = 0; r < MP; ++r) q[j][r] = qreg[j][r];
+      } else {
+        load_slot<MP, LC>(Qs + size_t(k - p.N - 1) * VEC, lane, q);
+      }
+      double ea[LC][MP], eb[LC][MP];
+      if (st.y <= p.N) gather_tip<MP, LC>(p, st.y, sc, lc, ea);
+      else load_slot<MP, LC>(E + size_t(st.y - p.N - 1) * VEC, lane, ea);
+      if (st.z <= p.N) gather_tip<MP, LC>(p, st.z, sc, lc, eb);
+      else load_slot<MP, LC>(E + size_t(st.z - p.N - 1) * VEC, lane, eb);
+
+      // denominator L_s e^{-S}: identical for both children (Eq. 8)
+      double den = 0.0;
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        double d = 0.0;
+#pragma unroll
+        for (int r = 0; r < MP; ++r) d = fma(q[j][r] * ea[j][r], eb[j][r], d);
+        den = fma(cw[j], d, den);
+      }
+      den = group_sum(den, G);
+
+      auto child = [&](const int x, const double(&ex_)[LC][MP], const double(&ey)[LC][MP]) {
+        const bool need_q = x > p.N || p.cap_pre != nullptr;
+        const double* Qm = p.qtab + size_t(p.qidx[x]) * MP * MP;
+        double num = 0.0, num2 = 0.0;
+        double qx[LC][MP];
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          double top[MP];
+#pragma unroll
+          for (int r = 0; r < MP; ++r) top[r] = q[j][r] * ey[j][r];
+          double qe[MP];
+#pragma unroll
+          for (int r = 0; r < MP; ++r) {
+            double a = 0.0;
+#pragma unroll
+            for (int c = 0; c < MP; ++c) a = fma(__ldg(Qm + r * MP + c), ex_[j][c], a);
+            qe[r] = a;
+          }
+          double d1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < MP; ++r) d1 = fma(top[r], qe[r], d1);
+          num = fma(crw[j], d1, num);
+          if (p.hess) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int r = 0; r < MP; ++r) {
+              double a = 0.0;
+#pragma unroll
+              for (int c = 0; c < MP; ++c) a = fma(__ldg(Qm + r * MP + c), qe[c], a);
+              d2 = fma(top[r], a, d2);
+            }
+            num2 = fma(cr2w[j], d2, num2);
+          }
+          if (need_q) {
+            // q_x = P_x^T top (engine.hpp:249-250): column c of P dotted with top
+            const double2* T =
+                reinterpret_cast<const double2*>(p.tc + (size_t(x - 1) * p.L + lc[j]) * p.NC * MP);
+#pragma unroll
+            for (int c = 0; c < MP; ++c) {
+              double a = 0.0;
+#pragma unroll
+              for (int h = 0; h < MP / 2; ++h) {
+                const double2 col = __ldg(T + c * (MP / 2) + h);
+                a = fma(col.x, top[2 * h], a);
+                a = fma(col.y, top[2 * h + 1], a);
+              }
+              qx[j][c] = a;
+            }
+          }
+        }
+        num = group_sum(num, G);
+        const double r1 = num / den;
+        const double gv = warp_sum(owner ? w * r1 : 0.0);
+        if (lane == 0) A[x] += gv;
+        if (p.hess) {
+          num2 = group_sum(num2, G);
+          const double r2 = num2 / den;
+          const double hv = warp_sum(owner ? w * (r2 - r1 * r1) : 0.0);
+          if (lane == 0) A[p.B + x] += hv;
+        }
+        if (need_q) {
+          const int exq = rescale<MP, LC>(qx, G, p.thr, p.force, p.disable);
+          if (p.cap_pre && valid) {
+#pragma unroll
+            for (int j = 0; j < LC; ++j)
+              if (creal[j])
+                for (int r = 0; r < MP; ++r) p.cap_pre[((size_t(x) * p.L + lc[j]) * p.P + s) * MP + r] = qx[j][r];
+            if (g == 0) p.cap_pre_exp[size_t(x) * p.P + s] = exq;
+          }
+          if (x > p.N) {
+            if (x == st.w) {
+#pragma unroll
+              for (int j = 0; j < LC; ++j)
+#pragma unroll
+                for (int r = 0; r < MP; ++r) qreg[j][r] = qx[j][r];
+              qnode = x;
+            } else {
+              store_slot<MP, LC>(Qs + size_t(x - p.N - 1) * VEC, lane, qx);
+            }
+          }
+        }
+      };
+      child(st.y, ea, eb);
+      child(st.z, eb, ea);
+    }
+  }
+}
+
+}  // namespace pgk

@@ -1,0 +1,142 @@
+"""Seeded synthetic workloads for the BASELINE.json configs.
+
+The paper's WNV/LASV/DENV alignments are not available; these generators
+produce inputs with the configs' shapes and value distributions: Yule trees
+numbered like parse_newick, model parameters drawn as the config states,
+forward simulation down the tree (alignment.hpp:243-286 semantics with
+per-block RNG streams so it parallelises), optional gaps, then first-occurrence
+pattern compression.  Input generation only — never inside a timed region.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as _L
+from ._lib import check, lib, ptr
+
+# name -> (tips, model_kind, categories, alpha, sites, branch_mean, clock, dt_mean, rate_scale, rate_sd, gaps)
+CONFIGS = {
+    "C1": dict(tips=64, model_kind=0, categories=1, gamma_alpha=1.0, sites=1000, branch_mean=0.02),
+    "C2": dict(tips=512, model_kind=1, categories=4, gamma_alpha=0.5, sites=20000, branch_mean=0.01,
+               gap_fraction=0.02),
+    "C3": dict(tips=2048, model_kind=2, categories=4, gamma_alpha=0.5, sites=1000000, clock=1, dt_mean=5.0,
+               rate_scale=1e-3, rate_sd=0.3),
+    "C4": dict(tips=1000, model_kind=3, categories=4, gamma_alpha=0.5, sites=200000, branch_mean=0.05),
+    "C5": dict(tips=256, model_kind=4, categories=4, gamma_alpha=0.5, sites=400000, branch_mean=0.1),
+}
+DESCRIPTIONS = {
+    "C1": "HKY85 k=2 pi=(.3,.2,.2,.3), L=1, Yule-64, b~Exp(0.02), 1000 columns",
+    "C2": "GTR+G4(0.5), Yule-512, b~Exp(0.01), 20000 columns, 2% gaps",
+    "C3": "non-reversible 4-state+G4(0.5), Yule-2048, clock rates 1e-3*exp(N(0,.3^2)) x dt~Exp(5), 1e6 columns",
+    "C4": "AA-20 reversible+G4(0.5), Yule-1000, b~Exp(0.05), 2e5 columns",
+    "C5": "GY94 codon (w=.3,k=2)+G4(0.5), Yule-256, b~Exp(0.1), 4e5 columns",
+}
+
+
+@dataclass
+class Instance:
+    name: str
+    tip_count: int
+    parent: np.ndarray       # [2N]
+    children: np.ndarray     # [2N, 2]
+    post_order: np.ndarray   # [2N-1]
+    branch_lengths: np.ndarray  # [2N-2]
+    durations: np.ndarray    # [2N-2] (zeros unless clock)
+    branch_rates: np.ndarray  # [2N-2] (zeros unless clock)
+    q: np.ndarray
+    pi: np.ndarray
+    reversible: bool
+    cat_rates: np.ndarray
+    cat_probs: np.ndarray
+    codes: np.ndarray        # [N, P] int8, -1 missing
+    weights: np.ndarray      # [P] int64
+    clock: bool = False
+
+    @property
+    def states(self):
+        return int(self.q.shape[0])
+
+    @property
+    def patterns(self):
+        return int(self.weights.shape[0])
+
+    @property
+    def branches(self):
+        return 2 * self.tip_count - 2
+
+    def labels(self):
+        return [""] + [f"t{i}" for i in range(1, self.tip_count + 1)] + [""] * (self.tip_count - 1)
+
+    def slice_patterns(self, p0, p1) -> "Instance":
+        import dataclasses
+        return dataclasses.replace(self, codes=np.ascontiguousarray(self.codes[:, p0:p1]),
+                                   weights=np.ascontiguousarray(self.weights[p0:p1]))
+
+
+def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int | None = None,
+             threads: int = 0) -> Instance:
+    cfg = dict(CONFIGS[name])
+    spec = _L.SynthSpec()
+    spec.tips = tips or cfg["tips"]
+    spec.model_kind = cfg["model_kind"]
+    spec.categories = cfg["categories"]
+    spec.gamma_alpha = cfg.get("gamma_alpha", 1.0)
+    spec.sites = sites or cfg["sites"]
+    spec.branch_mean = cfg.get("branch_mean", 0.01)
+    spec.clock = cfg.get("clock", 0)
+    spec.dt_mean = cfg.get("dt_mean", 1.0)
+    spec.rate_scale = cfg.get("rate_scale", 1.0)
+    spec.rate_sd = cfg.get("rate_sd", 0.0)
+    spec.gap_fraction = cfg.get("gap_fraction", 0.0)
+    spec.seed = seed
+    spec.threads = threads
+    L = lib()
+    h = C.c_void_p()
+    P = C.c_int()
+    m = C.c_int()
+    check(L.pg_synth_create(C.byref(spec), C.byref(h), C.byref(P), C.byref(m)))
+    try:
+        N = spec.tips
+        n = 2 * N - 1
+        parent = np.zeros(n + 1, np.int32)
+        children = np.zeros(2 * (n + 1), np.int32)
+        post = np.zeros(n, np.int32)
+        blen = np.zeros(n - 1)
+        dt = np.zeros(n - 1)
+        rr = np.zeros(n - 1)
+        check(L.pg_synth_tree(h, ptr(parent, C.c_int32), ptr(children, C.c_int32), ptr(post, C.c_int32),
+                              ptr(blen, C.c_double), ptr(dt, C.c_double), ptr(rr, C.c_double)))
+        mm = m.value
+        q = np.zeros(mm * mm)
+        pi = np.zeros(mm)
+        rev = C.c_int()
+        cr = np.zeros(spec.categories)
+        cp = np.zeros(spec.categories)
+        check(L.pg_synth_model(h, ptr(q, C.c_double), ptr(pi, C.c_double), C.byref(rev), ptr(cr, C.c_double),
+                               ptr(cp, C.c_double)))
+        codes = np.zeros((N, P.value), np.int8)
+        w = np.zeros(P.value, np.int64)
+        check(L.pg_synth_patterns(h, ptr(codes, C.c_int8), ptr(w, C.c_int64)))
+    finally:
+        L.pg_synth_free(h)
+    return Instance(name, N, parent, children.reshape(n + 1, 2), post, blen, dt, rr, q.reshape(mm, mm), pi,
+                    bool(rev.value), cr, cp, codes, w, bool(spec.clock))
+
+
+def engine_for(inst: Instance, options=None):
+    """Builds a LikelihoodEngine over an Instance (tips bound in order)."""
+    from .api import LikelihoodEngine, RateCategories, SitePatternAlignment, SubstitutionModel, Tree
+
+    labels = inst.labels()
+    tree = Tree(inst.tip_count, inst.parent, inst.children,
+                np.concatenate([[0.0], inst.branch_lengths, [0.0]]), labels, inst.post_order)
+    aln = SitePatternAlignment(labels[1:inst.tip_count + 1], inst.states, inst.codes, inst.weights)
+    model = SubstitutionModel(inst.q, inst.pi, inst.reversible)
+    cats = RateCategories(inst.cat_rates, inst.cat_probs)
+    eng = LikelihoodEngine(tree, aln, model, cats, options)
+    if inst.clock:
+        eng.set_clock_durations(inst.durations)
+    return eng
