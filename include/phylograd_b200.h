@@ -101,7 +101,7 @@ int pg_set_categories(pg_engine* e, int category_count, const double* rates, con
 int pg_set_branch_lengths(pg_engine* e, const double* b);
 /* Same, reading a DEVICE pointer (no host round trip). */
 int pg_set_branch_lengths_device(pg_engine* e, const double* b_device);
-int pg_get_branch_lengths(const pg_engine* e, double* b);
+int pg_get_branch_lengths(pg_engine* e, double* b);
 
 /* clock.hpp:42-55 / cli.hpp:429-440: calendar durations dt_i = t_i - t_pa(i)
  * used by PG_EVAL_RATE_GRAD (d logL / d r_i = dt_i g_i, b_i = r_i dt_i). */
@@ -140,6 +140,10 @@ void pg_invalidate_caches(pg_engine* e);
  * launch geometry. */
 int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states);
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms);
+/* Per-evaluation CUDA-event timing on the engine stream: returns the number of
+ * evaluations recorded since the previous call and the summed device ms of the
+ * walk kernel and of whole evaluations, then resets and (dis)arms recording. */
+int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total, double* eval_ms_total);
 
 /* ---- setup-side formats either side of the path ---- */
 /* tree.hpp:144-289 parse_newick: two calls — first with arrays NULL to learn

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
+#include <limits>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -91,7 +93,11 @@ struct pg_engine {
   std::vector<double> rates, probs;
   // lengths
   std::vector<double> blen, dt;
-  bool has_dt = false;
+  bool has_dt = false, blen_host_stale = false;
+  // per-evaluation CUDA events around the walk kernel and the whole evaluation
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // 3 per evaluation: start, walk begin, walk end
+  size_t tev_used = 0;
 
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
@@ -119,6 +125,7 @@ struct pg_engine {
   int pending_flags = 0;
 
   ~pg_engine() {
+    for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
     if (h_out) cudaFreeHost(h_out);
     if (h_err) cudaFreeHost(h_err);
     if (ev0) cudaEventDestroy(ev0);
@@ -360,8 +367,16 @@ struct pg_engine {
     invalidate();
   }
 
+  void sync_host_blen() {
+    if (!blen_host_stale) return;
+    PG_CUDA(cudaMemcpyAsync(blen.data(), d_blen.p, sizeof(double) * size_t(B()), cudaMemcpyDeviceToHost, stream));
+    PG_CUDA(cudaStreamSynchronize(stream));
+    blen_host_stale = false;
+  }
+
   void set_branch_lengths(const double* b) {
     if (N == 0) throw std::logic_error("engine: set the topology first");
+    sync_host_blen();
     bool same = true;
     for (int i = 0; i < B(); ++i) {
       if (!std::isfinite(b[i]) || b[i] < 0.0)
@@ -381,7 +396,7 @@ struct pg_engine {
     set_device();
     d_blen.ensure(size_t(B()));
     PG_CUDA(cudaMemcpyAsync(d_blen.p, b, sizeof(double) * size_t(B()), cudaMemcpyDeviceToDevice, stream));
-    PG_CUDA(cudaMemcpyAsync(blen.data(), b, sizeof(double) * size_t(B()), cudaMemcpyDeviceToHost, stream));
+    blen_host_stale = true;
     tc_dirty = true;
     invalidate();
   }
@@ -508,15 +523,29 @@ struct pg_engine {
     int launches = 0;
     PG_CUDA(cudaMemsetAsync(d_err.p, 0x7f, 3 * sizeof(int), stream));  // INT_MAX-ish sentinel
     PG_CUDA(cudaEventRecord(ev0, stream));
+    cudaEvent_t* te = nullptr;
+    if (timing) {
+      if (tev_used + 3 > tev.size())
+        for (int k = 0; k < 3; ++k) {
+          cudaEvent_t ev;
+          PG_CUDA(cudaEventCreate(&ev));
+          tev.push_back(ev);
+        }
+      te = &tev[tev_used];
+      tev_used += 3;
+      PG_CUDA(cudaEventRecord(te[0], stream));
+    }
     if (tc_dirty) {
       launch_tc();
       ++launches;
       tc_dirty = false;
     }
     PG_CUDA(cudaEventRecord(ev1, stream));
+    if (te) PG_CUDA(cudaEventRecord(te[1], stream));
     launch_walk(want_grad, want_hess);
     ++launches;
     PG_CUDA(cudaEventRecord(ev2, stream));
+    if (te) PG_CUDA(cudaEventRecord(te[2], stream));
     const int width = want_hess ? accw : 1 + B();
     double* out = out_device ? out_device : d_out.p;
     pgk::reduce_kernel<<<(width + 255) / 256, 256, 0, stream>>>(
@@ -544,7 +573,10 @@ struct pg_engine {
   void evaluate(int flags, double* ll_out, double* g_out, double* h_out_) {
     if ((flags & PG_EVAL_REQUIRE_POST) && !post_valid)
       throw std::logic_error("engine: pre-order pass requires a current post-order pass");
-    if (flags & PG_EVAL_FORCE) invalidate();
+    if (flags & PG_EVAL_FORCE) {
+      invalidate();
+      tc_dirty = true;
+    }
     const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
     const bool want_hess = flags & PG_EVAL_HESS;
     const bool rate = flags & PG_EVAL_RATE_GRAD;
@@ -732,8 +764,12 @@ int pg_set_branch_lengths_device(pg_engine* e, const double* b_device) {
   return guarded([&] { e->set_branch_lengths_device(b_device); });
 }
 
-int pg_get_branch_lengths(const pg_engine* e, double* b) {
-  return guarded([&] { std::copy(e->blen.begin(), e->blen.end(), b); });
+int pg_get_branch_lengths(pg_engine* e, double* b) {
+  return guarded([&] {
+    e->set_device();
+    e->sync_host_blen();
+    std::copy(e->blen.begin(), e->blen.end(), b);
+  });
 }
 
 int pg_set_clock_durations(pg_engine* e, const double* dt) {
@@ -805,20 +841,46 @@ int pg_get_partials(pg_engine* e, int node, int category, double* post, double* 
         for (int s = 0; s < P; ++s)
           spre[size_t(x) * P + s] = spre[size_t(st.x) * P + s] + spost[size_t(y) * P + s] + eq[size_t(x) * P + s];
       }
+    // Present values like the reference (engine.hpp:396-414): unscaled when the
+    // true partial's peak is >= the rescaling threshold, otherwise normalised
+    // with the remaining log scaler (true = value * exp(scaler)).
     const double ln2 = 0.6931471805599453;
-    for (int s = 0; s < P; ++s) {
-      for (int j = 0; j < m; ++j) {
-        if (post) {
-          if (node <= e->N) post[size_t(s) * m + j] = std::numeric_limits<double>::quiet_NaN();  // tips: dense tip data lives on the host
-          else post[size_t(s) * m + j] = cp[((size_t(node) * e->L + category) * P + s) * MP + j];
-        }
-        if (pre) {
-          if (node == n) pre[size_t(s) * m + j] = e->pi[size_t(j)];
-          else pre[size_t(s) * m + j] = cq[((size_t(node) * e->L + category) * P + s) * MP + j];
-        }
+    const double thr = e->opt.rescaling_threshold;
+    const int L = e->L;
+    auto emit = [&](const std::vector<double>& cap, long E, int s, double* out, double* scaler, bool is_pre) {
+      double pk = 0.0;
+      for (int l = 0; l < L; ++l)
+        for (int j = 0; j < m; ++j) pk = std::max(pk, cap[((size_t(node) * L + l) * P + s) * MP + j]);
+      const double true_pk = std::ldexp(pk, int(std::max<long>(std::min<long>(E, 4000), -4000)));
+      const bool fold = e->opt.disable_rescaling || pk == 0.0 || (true_pk >= thr && std::isfinite(true_pk));
+      long keepE = 0;
+      if (!fold) {
+        int ex;
+        std::frexp(pk, &ex);
+        keepE = E + ex;  // normalise peak into [0.5, 1)
       }
-      if (post_scaler) post_scaler[s] = double(spost[size_t(node) * P + s]) * ln2;
-      if (pre_scaler) pre_scaler[s] = double(spre[size_t(node) * P + s]) * ln2;
+      for (int j = 0; j < m; ++j) {
+        const double v = cap[((size_t(node) * L + category) * P + s) * MP + j];
+        if (out) out[size_t(s) * m + j] = std::ldexp(v, int(std::max<long>(std::min<long>(E - keepE, 4000), -4000)));
+      }
+      if (scaler) *scaler = double(keepE) * ln2;
+      (void)is_pre;
+    };
+    for (int s = 0; s < P; ++s) {
+      if (node <= e->N) {
+        if (post)
+          for (int j = 0; j < m; ++j) post[size_t(s) * m + j] = std::numeric_limits<double>::quiet_NaN();
+        if (post_scaler) post_scaler[s] = 0.0;
+      } else {
+        emit(cp, spost[size_t(node) * P + s], s, post, post_scaler ? post_scaler + s : nullptr, false);
+      }
+      if (node == n) {
+        if (pre)
+          for (int j = 0; j < m; ++j) pre[size_t(s) * m + j] = e->pi[size_t(j)];
+        if (pre_scaler) pre_scaler[s] = 0.0;
+      } else {
+        emit(cq, spre[size_t(node) * P + s], s, pre, pre_scaler ? pre_scaler + s : nullptr, true);
+      }
     }
   });
 }
@@ -833,7 +895,10 @@ int pg_get_site_log_likelihoods(pg_engine* e, double* out) {
 
 uint64_t pg_node_visits(const pg_engine* e) { return e->visits; }
 void pg_reset_node_visits(pg_engine* e) { e->visits = 0; }
-void pg_invalidate_caches(pg_engine* e) { e->invalidate(); }
+void pg_invalidate_caches(pg_engine* e) {
+  e->invalidate();
+  e->tc_dirty = true;  // the reference recomputes trans_ in every post pass (engine.hpp:197-201)
+}
 
 int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states) {
   return guarded([&] {
@@ -841,6 +906,27 @@ int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lan
     if (total_warps) *total_warps = e->TW;
     if (lanes_per_pattern) *lanes_per_pattern = e->G;
     if (padded_states) *padded_states = e->MP;
+  });
+}
+
+int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total, double* eval_ms_total) {
+  return guarded([&] {
+    e->set_device();
+    PG_CUDA(cudaStreamSynchronize(e->stream));
+    const int n = int(e->tev_used / 3);
+    double w = 0.0, t = 0.0;
+    for (int i = 0; i < n; ++i) {
+      float a = 0.f, b = 0.f;
+      PG_CUDA(cudaEventElapsedTime(&a, e->tev[size_t(3 * i + 1)], e->tev[size_t(3 * i + 2)]));
+      PG_CUDA(cudaEventElapsedTime(&b, e->tev[size_t(3 * i)], e->tev[size_t(3 * i + 2)]));
+      w += a;
+      t += b;
+    }
+    if (evaluations) *evaluations = n;
+    if (walk_ms_total) *walk_ms_total = w;
+    if (eval_ms_total) *eval_ms_total = t;
+    e->tev_used = 0;
+    e->timing = enable != 0;
   });
 }
 

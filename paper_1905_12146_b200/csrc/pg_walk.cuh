@@ -130,6 +130,48 @@ __device__ __forceinline__ int rescale(double (&v)[LC][MP], int G, double thr, i
   return ex;
 }
 
+// Exact power-of-two normalisation of one pattern's LC x MP block (group max
+// over the G lanes of the pattern brought into [0.5, 1)).  Returns the
+// exponent removed.  Used by the pre-order pass, whose gradient ratio is
+// invariant to per-pattern scaling of q_k, e_a and e_b separately; keeping
+// all three near 1 keeps q o e_a o e_b far from the subnormal range.
+template <int MP, int LC>
+__device__ __forceinline__ int normalize(double (&v)[LC][MP], int G) {
+  double pk = 0.0;
+#pragma unroll
+  for (int j = 0; j < LC; ++j)
+#pragma unroll
+    for (int i = 0; i < MP; ++i) pk = fmax(pk, v[j][i]);
+  pk = group_max(pk, G);
+  const long long bits = __double_as_longlong(pk);
+  const int biased = int((bits >> 52) & 0x7ff);
+  if (pk <= 0.0 || biased == 0x7ff) return 0;  // zero, inf or NaN: leave alone
+  int ex;
+  if (biased == 0) {  // subnormal peak
+    frexp(pk, &ex);
+#pragma unroll
+    for (int j = 0; j < LC; ++j)
+#pragma unroll
+      for (int i = 0; i < MP; ++i) v[j][i] = ldexp(v[j][i], -ex);
+    return ex;
+  }
+  ex = biased - 1022;
+  if (ex == 0) return 0;
+  const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+  if (1023 - ex <= 0 || 1023 - ex >= 2047) {
+#pragma unroll
+    for (int j = 0; j < LC; ++j)
+#pragma unroll
+      for (int i = 0; i < MP; ++i) v[j][i] = ldexp(v[j][i], -ex);
+    return ex;
+  }
+#pragma unroll
+  for (int j = 0; j < LC; ++j)
+#pragma unroll
+    for (int i = 0; i < MP; ++i) v[j][i] *= sc;
+  return ex;
+}
+
 template <int MP, int LC>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_constant__ WalkParams p) {
   const int lane = threadIdx.x & 31;
@@ -273,6 +315,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
       else load_slot<MP, LC>(E + size_t(st.y - p.N - 1) * VEC, lane, ea);
       if (st.z <= p.N) gather_tip<MP, LC>(p, st.z, sc, lc, eb);
       else load_slot<MP, LC>(E + size_t(st.z - p.N - 1) * VEC, lane, eb);
+      const int nq = normalize<MP, LC>(q, G);
+      const int na = normalize<MP, LC>(ea, G);
+      const int nb = normalize<MP, LC>(eb, G);
 
       // denominator L_s e^{-S}: identical for both children (Eq. 8)
       double den = 0.0;
@@ -285,7 +330,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
       }
       den = group_sum(den, G);
 
-      auto child = [&](const int x, const double(&ex_)[LC][MP], const double(&ey)[LC][MP]) {
+      auto child = [&](const int x, const double(&ex_)[LC][MP], const double(&ey)[LC][MP], const int shift) {
         const bool need_q = x > p.N || p.cap_pre != nullptr;
         const double* Qm = p.qtab + size_t(p.qidx[x]) * MP * MP;
         double num = 0.0, num2 = 0.0;
@@ -346,7 +391,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
           if (lane == 0) A[p.B + x] += hv;
         }
         if (need_q) {
-          const int exq = rescale<MP, LC>(qx, G, p.thr, p.force, p.disable);
+          // q_x needs no threshold rescale: the next step normalises it.
+          // For the debug capture, record the total exponent removed
+          // relative to P^T(q_k o e_y) so scalers can be reconstructed.
+          const int exq = shift;
           if (p.cap_pre && valid) {
 #pragma unroll
             for (int j = 0; j < LC; ++j)
@@ -367,8 +415,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
           }
         }
       };
-      child(st.y, ea, eb);
-      child(st.z, eb, ea);
+      child(st.y, ea, eb, nq + nb);
+      child(st.z, eb, ea, nq + na);
     }
   }
 }
