@@ -1,0 +1,55 @@
+// C++ drop-in check: the reference's canonical call pattern (README.md
+// "Library sketch"; test_engine.cpp:24-35, :189-204) through the
+// phylograd_b200 facade.  Exit code 0 = pass.  Needs a GPU at run time.
+#include <cmath>
+#include <cstdio>
+
+#include "phylograd_b200/engine.hpp"
+
+using namespace phylograd_b200;
+
+static int failures = 0;
+static void expect(bool ok, const char* what) {
+  std::printf("%s: %s\n", ok ? "PASS" : "FAIL", what);
+  if (!ok) ++failures;
+}
+
+int main() {
+  Tree tree = parse_newick("(A:0.1,B:0.2);");
+  SubstitutionModel jc;
+  jc.q.assign(16, 1.0 / 3.0);
+  for (int i = 0; i < 4; ++i) jc.q[size_t(i * 4 + i)] = -1.0;
+  jc.pi.assign(4, 0.25);
+  auto aln = SitePatternAlignment::from_codes({"A", "B"}, {{0}, {1}}, 4);
+  LikelihoodEngine engine(tree, aln, jc, RateCategories::single());
+  const double same = 0.25 + 0.75 * std::exp(-4.0 * 0.3 / 3.0);
+  const double site = 0.25 * (1.0 - same) / 3.0;
+  expect(std::fabs(engine.log_likelihood() - std::log(site)) < 1e-14, "two-taxon JC logL");
+  GradientReport r = engine.branch_gradient(true);
+  const double g = std::exp(-0.4) / (0.75 * (1.0 - std::exp(-0.4)));
+  expect(std::fabs(r.branch_gradient[0] - g) < 1e-12 * g, "two-taxon JC gradient (branch 1)");
+  expect(std::fabs(r.branch_gradient[1] - g) < 1e-12 * g, "two-taxon JC gradient (branch 2)");
+  expect(r.hessian_diagonal.size() == 2, "hessian requested");
+  engine.reset_node_visits();
+  engine.invalidate_caches();
+  engine.branch_gradient();
+  expect(engine.node_visits() == 6, "node visits 2(2N-1)");
+  bool threw = false;
+  try {
+    engine.set_branch_lengths({-0.1, 0.2});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  expect(threw, "negative length rejected with std::invalid_argument");
+  threw = false;
+  try {
+    Tree other = parse_newick("(A:0.1,Mismatch:0.2);");
+    LikelihoodEngine bad(other, aln, jc, RateCategories::single());
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()).find("not found") != std::string::npos;
+  }
+  expect(threw, "unbound tip -> 'not found'");
+  auto cats = discrete_gamma_categories(0.5, 4);
+  expect(cats.count() == 4 && std::fabs(cats.rates[0] - 0.0290777) < 1e-6, "discrete gamma(0.5, 4)");
+  return failures == 0 ? 0 : 1;
+}
