@@ -140,6 +140,9 @@ void pg_invalidate_caches(pg_engine* e);
  * launch geometry. */
 int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states);
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms);
+/* Walk-kernel variant of the current geometry: 0 generic register-tiled
+ * walk_kernel<MP,LC>, 1 pipelined 4-state walk4_kernel. */
+int pg_engine_variant(const pg_engine* e);
 /* Per-evaluation CUDA-event timing on the engine stream: returns the number of
  * evaluations recorded since the previous call and the summed device ms of the
  * walk kernel and of whole evaluations, then resets and (dis)arms recording. */

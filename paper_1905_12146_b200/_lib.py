@@ -36,7 +36,7 @@ EXPORTS = [
     "pg_set_branch_lengths_device", "pg_get_branch_lengths", "pg_set_clock_durations", "pg_evaluate",
     "pg_evaluate_device", "pg_check_errors", "pg_set_stream", "pg_get_partials", "pg_get_site_log_likelihoods",
     "pg_node_visits", "pg_reset_node_visits", "pg_invalidate_caches", "pg_engine_info", "pg_last_walk_ms",
-    "pg_timing",
+    "pg_timing", "pg_engine_variant",
     "pg_newick_parse", "pg_compress_codes", "pg_compress_result", "pg_compress_free", "pg_discrete_gamma",
     "pg_synth_create", "pg_synth_tree", "pg_synth_model", "pg_synth_patterns", "pg_synth_free",
 ]
@@ -168,6 +168,7 @@ def _declare(L):
         "pg_engine_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
         "pg_last_walk_ms": (I, [P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "pg_timing": (I, [P, I, C.POINTER(I), C.POINTER(D), C.POINTER(D)]),
+        "pg_engine_variant": (I, [P]),
         "pg_newick_parse": (I, [C.c_char_p, C.POINTER(I), PI32, PI32, PD, PI32, C.c_char_p, C.c_int64]),
         "pg_compress_codes": (I, [I, C.c_int64, PI32, I, C.POINTER(P), C.POINTER(I)]),
         "pg_compress_result": (I, [P, PI32, PI64, PI32]),

@@ -18,6 +18,7 @@
 #include "pg_common.hpp"
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
+#include "pg_walk4.cuh"
 
 void* pg_walk_kernel_small(int MP, int LC);
 void* pg_walk_kernel_mid(int MP, int LC);
@@ -101,6 +102,8 @@ struct pg_engine {
 
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
+  bool use_walk4 = false;
+  size_t walk_smem = 0;
   bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
 
   // device state
@@ -459,11 +462,19 @@ struct pg_engine {
     const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;
     LC = std::min(maxLC, pow2ceil(L));
     // Prefer more, smaller tiles when the pattern count cannot fill the GPU.
-    while (LC > 1 && (int64_t(P) * pow2ceil((L + LC - 1) / LC)) / 32 < int64_t(num_sms) * 8) LC >>= 1;
+    while (LC > 1 && (int64_t(P) * pow2ceil((L + LC - 1) / LC)) / 32 < int64_t(num_sms)) LC >>= 1;
     G = pow2ceil((L + LC - 1) / LC);
     if (G > 32) throw NotSupported("engine: too many rate categories for the lane layout");
     const int TP = 32 / G;
     ntiles = (P + TP - 1) / TP;
+    // specialised pipelined 4-state kernel (pg_walk4.cuh)
+    use_walk4 = MP == 4 && LC == 4 && G == 1 && L <= 4 && !opt.capture_partials;
+    walk_smem = 0;
+    if (use_walk4) {
+      const size_t tcb = size_t(L) * NC * 4;
+      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * 256 + 3 * (tcb / 2)) * sizeof(double2);
+      if (walk_smem > 200 * 1024) use_walk4 = false, walk_smem = 0;
+    }
     const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
     const size_t vec = size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
@@ -630,11 +641,14 @@ void* select_walk(int MP, int LC) {
 }  // namespace
 
 int pg_engine::walk_max_blocks_per_sm() {
-  const int mp = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
-  const int maxLC = mp == 4 ? 4 : mp == 8 ? 2 : 1;
   int nb = 0;
-  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_walk(mp, std::min(maxLC, pow2ceil(L))),
-                                                        pgk::kWarpsPerBlock * 32, 0));
+  if (use_walk4) {
+    PG_CUDA(cudaFuncSetAttribute(pgk::walk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pgk::walk4_kernel, pgk::kWarpsPerBlock * 32,
+                                                          walk_smem));
+  } else {
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_walk(MP, LC), pgk::kWarpsPerBlock * 32, 0));
+  }
   return std::max(nb, 1);
 }
 
@@ -701,6 +715,18 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   p.disable = opt.disable_rescaling;
   p.do_pre = do_pre ? 1 : 0;
   p.hess = do_hess ? 1 : 0;
+  if (use_walk4) {
+    pgk::Walk4Params p4{};
+    p4.p = p;
+    p4.homogeneous = branch_q.empty() ? 1 : 0;
+    for (int i = 0; i < 4; ++i) {
+      p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
+      for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
+    }
+    pgk::walk4_kernel<<<unsigned(TW / pgk::kWarpsPerBlock), pgk::kWarpsPerBlock * 32, walk_smem, stream>>>(p4);
+    PG_CUDA(cudaGetLastError());
+    return;
+  }
   void* fn = select_walk(MP, LC);
   void* args[] = {&p};
   PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args, 0,
@@ -929,6 +955,8 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
     e->timing = enable != 0;
   });
 }
+
+int pg_engine_variant(const pg_engine* e) { return e->use_walk4 ? 1 : 0; }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {
   return guarded([&] {

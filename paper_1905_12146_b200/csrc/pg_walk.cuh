@@ -111,30 +111,14 @@ __device__ __forceinline__ void gather_tip(const WalkParams& p, int node, int sc
   }
 }
 
-template <int MP, int LC>
-__device__ __forceinline__ int rescale(double (&v)[LC][MP], int G, double thr, int force, int disable) {
-  double pk = 0.0;
-#pragma unroll
-  for (int j = 0; j < LC; ++j)
-#pragma unroll
-    for (int i = 0; i < MP; ++i) pk = fmax(pk, v[j][i]);
-  pk = group_max(pk, G);
-  int ex = 0;
-  if (!disable && pk > 0.0 && (force || pk < thr)) {
-    frexp(pk, &ex);
-#pragma unroll
-    for (int j = 0; j < LC; ++j)
-#pragma unroll
-      for (int i = 0; i < MP; ++i) v[j][i] = ldexp(v[j][i], -ex);
-  }
-  return ex;
-}
-
 // Exact power-of-two normalisation of one pattern's LC x MP block (group max
 // over the G lanes of the pattern brought into [0.5, 1)).  Returns the
-// exponent removed.  Used by the pre-order pass, whose gradient ratio is
-// invariant to per-pattern scaling of q_k, e_a and e_b separately; keeping
-// all three near 1 keeps q o e_a o e_b far from the subnormal range.
+// exponent removed.  Post-order partials are normalised at every internal
+// node (the reference rescales by the peak only below 1e-150, engine.hpp:
+// 396-414; scaling by 2^k is exact, so values differ from the reference only
+// by that bookkeeping, which logL = log(mix) + S ln 2 undoes).  Pre-order
+// partials are normalised when produced: the gradient ratio is invariant to
+// it, and keeping q ~ 1 keeps q o e_a o e_b away from the subnormal range.
 template <int MP, int LC>
 __device__ __forceinline__ int normalize(double (&v)[LC][MP], int G) {
   double pk = 0.0;
@@ -235,7 +219,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
       for (int j = 0; j < LC; ++j)
 #pragma unroll
         for (int q = 0; q < MP; ++q) x[j][q] *= y[j][q];
-      const int ex = rescale<MP, LC>(x, G, p.thr, p.force, p.disable);
+      const int ex = p.disable ? 0 : normalize<MP, LC>(x, G);
       S += ex;
       if (p.cap_post && valid) {
 #pragma unroll
@@ -315,9 +299,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
       else load_slot<MP, LC>(E + size_t(st.y - p.N - 1) * VEC, lane, ea);
       if (st.z <= p.N) gather_tip<MP, LC>(p, st.z, sc, lc, eb);
       else load_slot<MP, LC>(E + size_t(st.z - p.N - 1) * VEC, lane, eb);
-      const int nq = normalize<MP, LC>(q, G);
-      const int na = normalize<MP, LC>(ea, G);
-      const int nb = normalize<MP, LC>(eb, G);
 
       // denominator L_s e^{-S}: identical for both children (Eq. 8)
       double den = 0.0;
@@ -330,7 +311,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
       }
       den = group_sum(den, G);
 
-      auto child = [&](const int x, const double(&ex_)[LC][MP], const double(&ey)[LC][MP], const int shift) {
+      auto child = [&](const int x, const double(&ex_)[LC][MP], const double(&ey)[LC][MP]) {
         const bool need_q = x > p.N || p.cap_pre != nullptr;
         const double* Qm = p.qtab + size_t(p.qidx[x]) * MP * MP;
         double num = 0.0, num2 = 0.0;
@@ -391,10 +372,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
           if (lane == 0) A[p.B + x] += hv;
         }
         if (need_q) {
-          // q_x needs no threshold rescale: the next step normalises it.
-          // For the debug capture, record the total exponent removed
-          // relative to P^T(q_k o e_y) so scalers can be reconstructed.
-          const int exq = shift;
+          // normalise q_x by an exact power of two (the gradient ratio is
+          // invariant to it); the exponent is recorded for the debug capture
+          const int exq = normalize<MP, LC>(qx, G);
           if (p.cap_pre && valid) {
 #pragma unroll
             for (int j = 0; j < LC; ++j)
@@ -415,8 +395,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) walk_kernel(const __grid_
           }
         }
       };
-      child(st.y, ea, eb, nq + nb);
-      child(st.z, eb, ea, nq + na);
+      child(st.y, ea, eb);
+      child(st.z, eb, ea);
     }
   }
 }
