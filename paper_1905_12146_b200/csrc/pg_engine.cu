@@ -18,7 +18,9 @@
 #include "pg_common.hpp"
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
-#include "pg_walk4.cuh"
+
+void* pg_walk4_kernel(bool homog, bool hess, int nc);
+int pg_walk4_nc(int nc);
 
 void* pg_walk_kernel_small(int MP, int LC);
 void* pg_walk_kernel_mid(int MP, int LC);
@@ -459,6 +461,7 @@ struct pg_engine {
   void prepare_geometry() {
     MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
+    int nc4 = 0;
     const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;
     LC = std::min(maxLC, pow2ceil(L));
     // Prefer more, smaller tiles when the pattern count cannot fill the GPU.
@@ -468,12 +471,13 @@ struct pg_engine {
     const int TP = 32 / G;
     ntiles = (P + TP - 1) / TP;
     // specialised pipelined 4-state kernel (pg_walk4.cuh)
-    use_walk4 = MP == 4 && LC == 4 && G == 1 && L <= 4 && !opt.capture_partials;
+    nc4 = MP == 4 ? pg_walk4_nc(NC) : 0;
+    use_walk4 = MP == 4 && LC == 4 && G == 1 && L == 4 && !opt.capture_partials && nc4 > 0;
     walk_smem = 0;
     if (use_walk4) {
+      NC = nc4;  // TC blocks padded with zero columns to the instantiated width
       const size_t tcb = size_t(L) * NC * 4;
       walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * 256 + 3 * (tcb / 2)) * sizeof(double2);
-      if (walk_smem > 200 * 1024) use_walk4 = false, walk_smem = 0;
     }
     const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
     const size_t vec = size_t(32) * LC * MP;
@@ -643,9 +647,14 @@ void* select_walk(int MP, int LC) {
 int pg_engine::walk_max_blocks_per_sm() {
   int nb = 0;
   if (use_walk4) {
-    PG_CUDA(cudaFuncSetAttribute(pgk::walk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pgk::walk4_kernel, pgk::kWarpsPerBlock * 32,
-                                                          walk_smem));
+    // occupancy of the heaviest variant (per-branch Q + Hessian) bounds the grid
+    for (int v = 0; v < 4; ++v) {
+      const void* fn = pg_walk4_kernel(v & 1, v & 2, NC);
+      PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
+      int b = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
+      nb = v == 0 ? b : std::min(nb, b);
+    }
   } else {
     PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_walk(MP, LC), pgk::kWarpsPerBlock * 32, 0));
   }
@@ -718,13 +727,14 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   if (use_walk4) {
     pgk::Walk4Params p4{};
     p4.p = p;
-    p4.homogeneous = branch_q.empty() ? 1 : 0;
     for (int i = 0; i < 4; ++i) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
     }
-    pgk::walk4_kernel<<<unsigned(TW / pgk::kWarpsPerBlock), pgk::kWarpsPerBlock * 32, walk_smem, stream>>>(p4);
-    PG_CUDA(cudaGetLastError());
+    void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC);
+    void* args[] = {&p4};
+    PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
+                             walk_smem, stream));
     return;
   }
   void* fn = select_walk(MP, LC);

@@ -226,7 +226,7 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
     if (r < m) {
       if (c < p.MP) {
         if (c < m) v = R[r * m + c];
-      } else {
+      } else if (c - p.MP < p.A) {  // columns past the last class are zero padding
         const double* a = p.amb + size_t(c - p.MP) * m;
         for (int j = 0; j < m; ++j) v = fma(R[r * m + j], a[j], v);
       }

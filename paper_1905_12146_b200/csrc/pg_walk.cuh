@@ -55,6 +55,13 @@ struct WalkParams {
   int force, disable, do_pre, hess;
 };
 
+// Parameters of the pipelined 4-state kernel (pg_walk4.cuh).
+struct Walk4Params {
+  WalkParams p;
+  double q[16];  // homogeneous generator (row-major), constant-bank operands
+  double pi[4];
+};
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
