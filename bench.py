@@ -45,6 +45,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=None, help="patterns in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period in the timed region (0: off)")
     return ap.parse_args()
 
 
@@ -94,18 +95,21 @@ def profiled_traffic(config):
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=100):
         self.index = index
+        self.period = period_ms
         self.samples = []
         self.proc = None
 
     def __enter__(self):
+        if self.period <= 0:
+            return self
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -272,7 +276,7 @@ def main():
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local, args.clock_ms) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
             step_device()

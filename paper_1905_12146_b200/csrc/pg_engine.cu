@@ -84,6 +84,7 @@ struct pg_engine {
   std::vector<int4> post_steps, pre_steps;
   // patterns
   int m_aln = 0, P = 0, A = 0;
+  int64_t Pc = 0;  // device row stride of the tip codes
   bool has_patterns = false;
   std::vector<double> amb;  // [A][m]
   // model
@@ -254,14 +255,18 @@ struct pg_engine {
     // MP depends on m; column index encoding: state s -> s, class a -> MP + a,
     // missing -> MP + na (an extra all-ones class, alignment.hpp:223-224).
     const int mp = mm <= 4 ? 4 : mm <= 8 ? 8 : mm <= 20 ? 20 : mm <= 32 ? 32 : 64;
-    std::vector<uint8_t> col(size_t(N) * size_t(np));
+    // device layout: tip-major rows padded to whole 32-pattern tiles so a
+    // warp tile's codes of one tip are 32 aligned bytes (cp.async staging)
+    const int64_t pc = (int64_t(np) + 31) / 32 * 32;
+    std::vector<uint8_t> col(size_t(N) * size_t(std::max<int64_t>(pc, 32)), 0);
     bool any_missing = false;
-    for (size_t i = 0; i < col.size(); ++i) {
-      const int c = codes[i];
-      if (c < -1 || c >= mm + na) throw std::invalid_argument("alignment: state code out of range");
-      if (c == -1) any_missing = true;
-      col[i] = uint8_t(c < 0 ? mp + na : c < mm ? c : mp + (c - mm));
-    }
+    for (int t = 0; t < N; ++t)
+      for (int s = 0; s < np; ++s) {
+        const int c = codes[size_t(t) * size_t(np) + size_t(s)];
+        if (c < -1 || c >= mm + na) throw std::invalid_argument("alignment: state code out of range");
+        if (c == -1) any_missing = true;
+        col[size_t(t) * size_t(pc) + size_t(s)] = uint8_t(c < 0 ? mp + na : c < mm ? c : mp + (c - mm));
+      }
     std::vector<double> ambv(size_t(na + 1) * mm, 1.0);
     for (int a = 0; a < na; ++a)
       for (int j = 0; j < mm; ++j) ambv[size_t(a) * mm + j] = ambig[size_t(a) * mm + j];
@@ -278,6 +283,7 @@ struct pg_engine {
     PG_CUDA(cudaStreamSynchronize(stream));
     m_aln = mm;
     P = np;
+    Pc = int64_t(std::max<int64_t>(pc, 32));
     A = na + 1;
     amb = ambv;
     has_patterns = true;
@@ -477,7 +483,7 @@ struct pg_engine {
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
       const size_t tcb = size_t(L) * NC * 4;
-      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * 256 + 3 * (tcb / 2)) * sizeof(double2);
+      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * 256 + 3 * (tcb / 2) + 4) * sizeof(double2);
     }
     const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
     const size_t vec = size_t(32) * LC * MP;
@@ -712,6 +718,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   }
   p.N = N;
   p.P = P;
+  p.Pc = Pc;
   p.L = L;
   p.G = G;
   p.NC = NC;

@@ -31,7 +31,7 @@ constexpr int kWarpsPerBlock = 4;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct WalkParams {
-  const uint8_t* codes;  // [N][P] tip column index into the TC table
+  const uint8_t* codes;  // [N][Pc] tip column index into the TC table (rows padded to 32)
   const double* weights; // [P]
   const double* tc;      // [B][L][NC][MP]: column c of P (c < MP) or P*ambiguity (c >= MP)
   const double* qtab;    // [nq][MP][MP] row-major generators
@@ -51,6 +51,7 @@ struct WalkParams {
   int* cap_post_exp;     // [(2N)][P]
   int* cap_pre_exp;
   int N, P, L, G, NC, nsteps, ntiles, accw, B;
+  long long Pc;  // row stride of codes (P rounded up to 32)
   double thr;
   int force, disable, do_pre, hess;
 };
@@ -104,7 +105,7 @@ __device__ __forceinline__ void store_slot(double* base, int lane, const double 
 template <int MP, int LC>
 __device__ __forceinline__ void gather_tip(const WalkParams& p, int node, int sc, const int (&lc)[LC],
                                            double (&v)[LC][MP]) {
-  const int col = p.codes[size_t(node - 1) * p.P + sc];
+  const int col = p.codes[size_t(node - 1) * size_t(p.Pc) + sc];
 #pragma unroll
   for (int j = 0; j < LC; ++j) {
     const double2* src =

@@ -30,6 +30,20 @@ __device__ __forceinline__ void cp16_ca(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp16_cg_hint(void* smem, const void* gmem, unsigned long long pol) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+// The line's data is dead: drop it from L2 without a DRAM write-back.
+__device__ __forceinline__ void discard_l2(const void* gmem) {
+  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
@@ -49,7 +63,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
   constexpr int MP = 4, L = 4;
   constexpr int TCB = L * NC * MP;           // doubles per node TC block
   constexpr int TCC = TCB / 2;               // double2 chunks per TC block
-  constexpr int STAGE = 3 * 256 + 3 * TCC;   // double2 per stage: 3 operand slots + 3 TC blocks
+  constexpr int STAGE = 3 * 256 + 3 * TCC + 4;  // double2 per stage: 3 operand slots, 3 TC blocks, 2x32 B codes
   constexpr size_t VEC = 512;                // doubles per node slot (32 lanes x 16)
   const WalkParams& p = P4.p;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -80,10 +94,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
   auto tcp = [&](int stage, int slot) -> const double* {
     return reinterpret_cast<const double*>(wsm + stage * STAGE + 3 * 256 + slot * TCC);
   };
+  const unsigned long long pol_first = policy_evict_first();
   auto stage_slot = [&](int stage, int slot, const double2* g) {
     double2* d = opp(stage, slot);
 #pragma unroll
     for (int q = 0; q < 8; ++q) cp16_cg(d + q * 32, g + q * 32);
+  };
+  // edge messages are read once in the pre pass: evict-first
+  auto stage_slot_once = [&](int stage, int slot, const double2* g) {
+    double2* d = opp(stage, slot);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cp16_cg_hint(d + q * 32, g + q * 32, pol_first);
+  };
+  // tile t's 32 code bytes of one tip: lanes 0,1 copy 16 B each
+  auto stage_codes = [&](int stage, int which, const uint8_t* row) {
+    if (lane < 2) cp16_ca(wsm + stage * STAGE + 3 * 256 + 3 * TCC + which * 2 + lane, row + 16 * lane);
+  };
+  auto code_of = [&](int stage, int which) -> int {
+    return reinterpret_cast<const uint8_t*>(wsm + stage * STAGE + 3 * 256 + 3 * TCC + which * 2)[lane];
   };
   auto stage_tc = [&](int stage, int slot, int node) {
     const double2* g = reinterpret_cast<const double2*>(p.tc) + size_t(node - 1) * TCC;
@@ -127,32 +155,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
     const bool valid = s < p.P;
     const int sc = valid ? s : p.P - 1;
     const double w = valid ? p.weights[sc] : 0.0;
-    const uint8_t* codes = p.codes + sc;
-    const size_t P = size_t(p.P);
+    const uint8_t* codes = p.codes + size_t(t) * 32;  // tile base; row stride Pc
+    const size_t P = size_t(p.Pc);
 
     // ------------------------------------------------ post-order pass (a)
     {
       int S = 0;
       double keep[L][4];
-      int cn0 = 0, cn1 = 0;
       auto issue = [&](int j, const int4 d, int last) {
         const int st = j & 1;
-        int c0 = 0, c1 = 0;
         if (d.y <= N) {
-          c0 = codes[size_t(d.y - 1) * P];
+          stage_codes(st, 0, codes + size_t(d.y - 1) * P);
           stage_tc(st, 1, d.y);
         } else if (d.y != last) {
           stage_slot(st, 0, Eb + size_t(d.y) * 256);
         }
         if (d.z <= N) {
-          c1 = codes[size_t(d.z - 1) * P];
+          stage_codes(st, 1, codes + size_t(d.z - 1) * P);
           stage_tc(st, 2, d.z);
         } else if (d.z != last) {
           stage_slot(st, 0, Eb + size_t(d.z) * 256);
         }
         if (d.x != root) stage_tc(st, 0, d.x);
-        cn0 = c0;
-        cn1 = c1;
       };
       int4 win = lane < n ? p.post[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.post[32 + lane] : make_int4(0, 0, 0, 0);
@@ -162,7 +186,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
       int last = -1;
       for (int i = 0; i < n; ++i) {
         const int4 d = dnext;
-        const int code0 = cn0, code1 = cn1;
         if (i + 1 < n) {
           const int li = (i + 1) & 31;
           if (li == 0) {
@@ -176,6 +199,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         cp_wait1();
         __syncwarp();
         const int st = i & 1;
+        const int code0 = d.y <= N ? code_of(st, 0) : 0;
+        const int code1 = d.z <= N ? code_of(st, 1) : 0;
         // p_k = e_c0 o e_c1 for all categories, then exponent normalisation
         double x[L][4];
         int hm = 0;
@@ -253,8 +278,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
             keep[j][1] = e1;
             keep[j][2] = e2;
             keep[j][3] = e3;
-            __stcg(dst + (2 * j) * 32, make_double2(e0, e1));
-            __stcg(dst + (2 * j + 1) * 32, make_double2(e2, e3));
+            __stcs(dst + (2 * j) * 32, make_double2(e0, e1));
+            __stcs(dst + (2 * j + 1) * 32, make_double2(e2, e3));
           }
           last = d.x;
         }
@@ -265,19 +290,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
 
     // ----------------------------------- pre-order pass + gradient (b)+(c)
     {
-      int cn0 = 0, cn1 = 0;
       auto issue = [&](int j, const int4 d, int prev_next) {
         const int st = j & 1;
-        int c0 = 0, c1 = 0;
         if (d.x != root && prev_next != d.x) stage_slot(st, 2, Qw + size_t(d.x) * 256);
-        if (d.y <= N) c0 = codes[size_t(d.y - 1) * P];
-        else stage_slot(st, 0, Eb + size_t(d.y) * 256);
-        if (d.z <= N) c1 = codes[size_t(d.z - 1) * P];
-        else stage_slot(st, 1, Eb + size_t(d.z) * 256);
+        if (d.y <= N) stage_codes(st, 0, codes + size_t(d.y - 1) * P);
+        else stage_slot_once(st, 0, Eb + size_t(d.y) * 256);
+        if (d.z <= N) stage_codes(st, 1, codes + size_t(d.z - 1) * P);
+        else stage_slot_once(st, 1, Eb + size_t(d.z) * 256);
         stage_tc(st, 0, d.y);
         stage_tc(st, 1, d.z);
-        cn0 = c0;
-        cn1 = c1;
       };
       double qreg[L][4];
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
@@ -288,7 +309,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
       int prev_next = 0;
       for (int i = 0; i < n; ++i) {
         const int4 d = dnext;
-        const int code0 = cn0, code1 = cn1;
         if (i + 1 < n) {
           const int li = (i + 1) & 31;
           if (li == 0) {
@@ -303,6 +323,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         __syncwarp();
         const int st = i & 1;
         const bool q_in_reg = prev_next == d.x;
+        const int code0 = d.y <= N ? code_of(st, 0) : 0;
+        const int code1 = d.z <= N ? code_of(st, 1) : 0;
+        // consumed scratch is dead: drop it from L2 without write-back
+        {
+          const char* base_e = reinterpret_cast<const char*>(p.escr + size_t(warp) * size_t(N - 1) * VEC);
+          const char* base_q = reinterpret_cast<const char*>(p.qscr + size_t(warp) * size_t(N - 1) * VEC);
+          if (d.y > N) discard_l2(base_e + size_t(d.y - N - 1) * 4096 + lane * 128);
+          if (d.z > N) discard_l2(base_e + size_t(d.z - N - 1) * 4096 + lane * 128);
+          if (d.x != root && !q_in_reg) discard_l2(base_q + size_t(d.x - N - 1) * 4096 + lane * 128);
+        }
         const bool a_int = d.y > N, b_int = d.z > N;
         double qa[L][4], qb[L][4];
         double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
