@@ -324,10 +324,14 @@ def main():
         step_e2e(i)
     barrier()
     t0 = time.perf_counter()
+    e2e_walk = []
     for i in range(args.steps):
         step_e2e(i)
+        if world == 1:
+            e2e_walk.append(round(eng.last_times_ms()[0], 2))
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
+    print(f"e2e walk ms per step: {e2e_walk}", file=sys.stderr)
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <cstring>
@@ -19,7 +20,11 @@
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
 
-void* pg_walk4_kernel(bool homog, bool hess, int nc);
+void* pg_walk4_kernel_lc4(bool homog, bool hess, int nc);
+void* pg_walk4_kernel_lc2(bool homog, bool hess, int nc);
+static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv) {
+  return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
+}
 int pg_walk4_nc(int nc);
 
 void* pg_walk_kernel_small(int MP, int LC);
@@ -106,6 +111,7 @@ struct pg_engine {
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
+  int walk4_lcv = 4;  // categories per lane of the 4-state kernel
   size_t walk_smem = 0;
   bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
 
@@ -482,8 +488,13 @@ struct pg_engine {
     walk_smem = 0;
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
+      walk4_lcv = 2;
+      if (const char* v = std::getenv("PG_WALK4_LCV")) walk4_lcv = std::atoi(v) == 4 ? 4 : 2;
+      G = 4 / walk4_lcv;
+      ntiles = (P + 32 / G - 1) / (32 / G);
       const size_t tcb = size_t(L) * NC * 4;
-      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * 256 + 3 * (tcb / 2) + 4) * sizeof(double2);
+      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
+                  sizeof(double2);
     }
     const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
     const size_t vec = size_t(32) * LC * MP;
@@ -655,7 +666,7 @@ int pg_engine::walk_max_blocks_per_sm() {
   if (use_walk4) {
     // occupancy of the heaviest variant (per-branch Q + Hessian) bounds the grid
     for (int v = 0; v < 4; ++v) {
-      const void* fn = pg_walk4_kernel(v & 1, v & 2, NC);
+      const void* fn = pg_walk4_kernel(v & 1, v & 2, NC, walk4_lcv);
       PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
@@ -738,7 +749,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
     }
-    void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC);
+    void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv);
     void* args[] = {&p4};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
                              walk_smem, stream));

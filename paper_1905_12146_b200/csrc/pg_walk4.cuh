@@ -58,13 +58,20 @@ __device__ __forceinline__ int peak_exponent(int hmax) {
 // 2^-ex as a double (exact; ex in [-1021, 1022]).
 __device__ __forceinline__ double pow2_neg(int ex) { return __hiloint2double((1023 - ex) << 20, 0); }
 
-template <bool HOMOG, bool HESS, int NC>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __grid_constant__ Walk4Params P4) {
+// LCV = categories per lane (4: one lane per pattern, 32 patterns per warp
+// tile; 2: two lanes per pattern, 16 patterns per tile, half the registers
+// and shared memory per warp -> more resident warps).
+template <bool HOMOG, bool HESS, int NC, int LCV>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (LCV == 4 ? 2 : 3))
+    walk4_kernel(const __grid_constant__ Walk4Params P4) {
   constexpr int MP = 4, L = 4;
+  constexpr int G = 4 / LCV;                 // lanes per pattern
+  constexpr int TP = 32 / G;                 // patterns per warp tile
   constexpr int TCB = L * NC * MP;           // doubles per node TC block
   constexpr int TCC = TCB / 2;               // double2 chunks per TC block
-  constexpr int STAGE = 3 * 256 + 3 * TCC + 4;  // double2 per stage: 3 operand slots, 3 TC blocks, 2x32 B codes
-  constexpr size_t VEC = 512;                // doubles per node slot (32 lanes x 16)
+  constexpr int VEC = 32 * LCV * MP;         // doubles per node slot of one warp
+  constexpr int SD2 = VEC / 2;               // double2 per node slot
+  constexpr int STAGE = 3 * SD2 + 3 * TCC + 4;  // double2 per stage: 3 operand slots, 3 TC blocks, 2x32 B codes
   const WalkParams& p = P4.p;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -74,51 +81,65 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
   const int N = p.N, root = 2 * N - 1;
   double2* wsm = reinterpret_cast<double2*>(smem_raw) + size_t(wib) * 2 * STAGE;
 
-  double cw[L], crw[L], cr2w[L];
+  const int g = lane & (G - 1), pl = lane / G;
+  double cw[LCV], crw[LCV], cr2w[LCV];
 #pragma unroll
-  for (int j = 0; j < L; ++j) {
-    const double w = p.probs[j], r = p.rates[j];
+  for (int j = 0; j < LCV; ++j) {
+    const double w = p.probs[g * LCV + j], r = p.rates[g * LCV + j];
     cw[j] = w;
     crw[j] = r * w;
     cr2w[j] = r * r * w;
   }
+  auto gsum = [&](double v) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+  };
+  auto gmaxi = [&](int v) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+  };
   // lane-offset bases of this warp's scratch (slot k at + (k - N - 1) * VEC)
-  const double2* Eb = reinterpret_cast<const double2*>(p.escr + size_t(warp) * size_t(N - 1) * VEC) + lane - 256 * (N + 1);
-  double2* Ew = reinterpret_cast<double2*>(p.escr + size_t(warp) * size_t(N - 1) * VEC) + lane - 256 * (N + 1);
-  double2* Qw = reinterpret_cast<double2*>(p.qscr + size_t(warp) * size_t(N - 1) * VEC) + lane - 256 * (N + 1);
+  const double2* Eb = reinterpret_cast<const double2*>(p.escr + size_t(warp) * size_t(N - 1) * VEC) + lane -
+                      size_t(SD2) * size_t(N + 1);
+  double2* Ew = reinterpret_cast<double2*>(p.escr + size_t(warp) * size_t(N - 1) * VEC) + lane -
+                size_t(SD2) * size_t(N + 1);
+  double2* Qw = reinterpret_cast<double2*>(p.qscr + size_t(warp) * size_t(N - 1) * VEC) + lane -
+                size_t(SD2) * size_t(N + 1);
   double* A = p.acc + size_t(warp) * p.accw;
   for (int i = lane; i < p.accw; i += 32) A[i] = 0.0;
   __syncwarp();
 
-  auto opp = [&](int stage, int slot) -> double2* { return wsm + stage * STAGE + slot * 256 + lane; };
+  auto opp = [&](int stage, int slot) -> double2* { return wsm + stage * STAGE + slot * SD2 + lane; };
   auto tcp = [&](int stage, int slot) -> const double* {
-    return reinterpret_cast<const double*>(wsm + stage * STAGE + 3 * 256 + slot * TCC);
+    return reinterpret_cast<const double*>(wsm + stage * STAGE + 3 * SD2 + slot * TCC);
   };
   const unsigned long long pol_first = policy_evict_first();
-  auto stage_slot = [&](int stage, int slot, const double2* g) {
+  auto stage_slot = [&](int stage, int slot, const double2* gs) {
     double2* d = opp(stage, slot);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) cp16_cg(d + q * 32, g + q * 32);
+    for (int q = 0; q < 2 * LCV; ++q) cp16_cg(d + q * 32, gs + q * 32);
   };
   // edge messages are read once in the pre pass: evict-first
-  auto stage_slot_once = [&](int stage, int slot, const double2* g) {
+  auto stage_slot_once = [&](int stage, int slot, const double2* gs) {
     double2* d = opp(stage, slot);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) cp16_cg_hint(d + q * 32, g + q * 32, pol_first);
+    for (int q = 0; q < 2 * LCV; ++q) cp16_cg_hint(d + q * 32, gs + q * 32, pol_first);
   };
-  // tile t's 32 code bytes of one tip: lanes 0,1 copy 16 B each
+  // the tile's TP code bytes of one tip (16 B chunks)
   auto stage_codes = [&](int stage, int which, const uint8_t* row) {
-    if (lane < 2) cp16_ca(wsm + stage * STAGE + 3 * 256 + 3 * TCC + which * 2 + lane, row + 16 * lane);
+    if (lane < TP / 16) cp16_ca(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2 + lane, row + 16 * lane);
   };
   auto code_of = [&](int stage, int which) -> int {
-    return reinterpret_cast<const uint8_t*>(wsm + stage * STAGE + 3 * 256 + 3 * TCC + which * 2)[lane];
+    return reinterpret_cast<const uint8_t*>(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2)[pl];
   };
   auto stage_tc = [&](int stage, int slot, int node) {
-    const double2* g = reinterpret_cast<const double2*>(p.tc) + size_t(node - 1) * TCC;
-    double2* d = wsm + stage * STAGE + 3 * 256 + slot * TCC;
+    const double2* gs = reinterpret_cast<const double2*>(p.tc) + size_t(node - 1) * TCC;
+    double2* d = wsm + stage * STAGE + 3 * SD2 + slot * TCC;
 #pragma unroll
     for (int c = 0; c < (TCC + 31) / 32; ++c)
-      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, g + c * 32 + lane);
+      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
   };
   // one category (4 doubles) of a lane's slot: double2 q = 2j, 2j+1
   auto read_cat = [&](const double2* src, int j, double (&v)[4]) {
@@ -129,7 +150,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
     v[3] = b.y;
   };
   auto gather_cat = [&](const double* tcs, int code, int j, double (&v)[4]) {
-    const double2* c = reinterpret_cast<const double2*>(tcs + (j * NC + code) * MP);
+    const double2* c = reinterpret_cast<const double2*>(tcs + ((g * LCV + j) * NC + code) * MP);
     const double2 a = c[0], b = c[1];
     v[0] = a.x;
     v[1] = a.y;
@@ -151,30 +172,31 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
 
   const int n = p.nsteps;
   for (int t = warp; t < p.ntiles; t += TW) {
-    const int s = t * 32 + lane;
+    const int s = t * TP + pl;
     const bool valid = s < p.P;
+    const bool owner = valid && g == 0;
     const int sc = valid ? s : p.P - 1;
     const double w = valid ? p.weights[sc] : 0.0;
-    const uint8_t* codes = p.codes + size_t(t) * 32;  // tile base; row stride Pc
+    const uint8_t* codes = p.codes + size_t(t) * TP;  // tile base; row stride Pc
     const size_t P = size_t(p.Pc);
 
     // ------------------------------------------------ post-order pass (a)
     {
       int S = 0;
-      double keep[L][4];
+      double keep[LCV][4];
       auto issue = [&](int j, const int4 d, int last) {
         const int st = j & 1;
         if (d.y <= N) {
           stage_codes(st, 0, codes + size_t(d.y - 1) * P);
           stage_tc(st, 1, d.y);
         } else if (d.y != last) {
-          stage_slot(st, 0, Eb + size_t(d.y) * 256);
+          stage_slot(st, 0, Eb + size_t(d.y) * SD2);
         }
         if (d.z <= N) {
           stage_codes(st, 1, codes + size_t(d.z - 1) * P);
           stage_tc(st, 2, d.z);
         } else if (d.z != last) {
-          stage_slot(st, 0, Eb + size_t(d.z) * 256);
+          stage_slot(st, 0, Eb + size_t(d.z) * SD2);
         }
         if (d.x != root) stage_tc(st, 0, d.x);
       };
@@ -202,10 +224,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         const int code0 = d.y <= N ? code_of(st, 0) : 0;
         const int code1 = d.z <= N ? code_of(st, 1) : 0;
         // p_k = e_c0 o e_c1 for all categories, then exponent normalisation
-        double x[L][4];
+        double x[LCV][4];
         int hm = 0;
 #pragma unroll
-        for (int j = 0; j < L; ++j) {
+        for (int j = 0; j < LCV; ++j) {
           double a[4], b[4];
           if (d.y <= N) gather_cat(tcp(st, 1), code0, j, a);
           else if (d.y == last) {
@@ -224,18 +246,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
           }
         }
         if (!p.disable) {
-          const int ex = peak_exponent(hm);
+          const int ex = peak_exponent(gmaxi(hm));
           if (ex != 0) {
             S += ex;
             if (ex <= 1022) {
               const double sc2 = pow2_neg(ex);
 #pragma unroll
-              for (int j = 0; j < L; ++j)
+              for (int j = 0; j < LCV; ++j)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) x[j][r] *= sc2;
             } else {
 #pragma unroll
-              for (int j = 0; j < L; ++j)
+              for (int j = 0; j < LCV; ++j)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) x[j][r] = ldexp(x[j][r], -ex);
             }
@@ -244,26 +266,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         if (d.x == root) {
           double mix = 0.0;
 #pragma unroll
-          for (int j = 0; j < L; ++j) {
+          for (int j = 0; j < LCV; ++j) {
             double dd = 0.0;
 #pragma unroll
             for (int r = 0; r < 4; ++r) dd = fma(P4.pi[r], x[j][r], dd);
             mix = fma(cw[j], dd, mix);
           }
+          mix = gsum(mix);
           const double ll = log(mix) + double(S) * 0.6931471805599453;
-          if (valid) {
+          if (owner) {
             if (!isfinite(mix)) atomicMin(&p.err[0], s);
             else if (mix <= 0.0) atomicMin(&p.err[1], s);
             if (p.site_ll) p.site_ll[s] = ll;
           }
-          const double v = warp_sum(valid ? w * ll : 0.0);
+          const double v = warp_sum(owner ? w * ll : 0.0);
           if (lane == 0) atomicAdd(A, v);
         } else {
           const double* T = tcp(st, 0);
-          double2* dst = Ew + size_t(d.x) * 256;
+          double2* dst = Ew + size_t(d.x) * SD2;
 #pragma unroll
-          for (int j = 0; j < L; ++j) {
-            const double2* Tl = reinterpret_cast<const double2*>(T + j * NC * MP);
+          for (int j = 0; j < LCV; ++j) {
+            const double2* Tl = reinterpret_cast<const double2*>(T + (g * LCV + j) * NC * MP);
             double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -292,15 +315,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
     {
       auto issue = [&](int j, const int4 d, int prev_next) {
         const int st = j & 1;
-        if (d.x != root && prev_next != d.x) stage_slot(st, 2, Qw + size_t(d.x) * 256);
+        if (d.x != root && prev_next != d.x) stage_slot(st, 2, Qw + size_t(d.x) * SD2);
         if (d.y <= N) stage_codes(st, 0, codes + size_t(d.y - 1) * P);
-        else stage_slot_once(st, 0, Eb + size_t(d.y) * 256);
+        else stage_slot_once(st, 0, Eb + size_t(d.y) * SD2);
         if (d.z <= N) stage_codes(st, 1, codes + size_t(d.z - 1) * P);
-        else stage_slot_once(st, 1, Eb + size_t(d.z) * 256);
+        else stage_slot_once(st, 1, Eb + size_t(d.z) * SD2);
         stage_tc(st, 0, d.y);
         stage_tc(st, 1, d.z);
       };
-      double qreg[L][4];
+      double qreg[LCV][4];
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
       int4 dnext = shfl4(win, 0);
@@ -326,21 +349,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         const int code0 = d.y <= N ? code_of(st, 0) : 0;
         const int code1 = d.z <= N ? code_of(st, 1) : 0;
         // consumed scratch is dead: drop it from L2 without write-back
-        {
+        if (lane < VEC / 16) {
           const char* base_e = reinterpret_cast<const char*>(p.escr + size_t(warp) * size_t(N - 1) * VEC);
           const char* base_q = reinterpret_cast<const char*>(p.qscr + size_t(warp) * size_t(N - 1) * VEC);
-          if (d.y > N) discard_l2(base_e + size_t(d.y - N - 1) * 4096 + lane * 128);
-          if (d.z > N) discard_l2(base_e + size_t(d.z - N - 1) * 4096 + lane * 128);
-          if (d.x != root && !q_in_reg) discard_l2(base_q + size_t(d.x - N - 1) * 4096 + lane * 128);
+          if (d.y > N) discard_l2(base_e + size_t(d.y - N - 1) * (VEC * 8) + lane * 128);
+          if (d.z > N) discard_l2(base_e + size_t(d.z - N - 1) * (VEC * 8) + lane * 128);
+          if (d.x != root && !q_in_reg) discard_l2(base_q + size_t(d.x - N - 1) * (VEC * 8) + lane * 128);
         }
         const bool a_int = d.y > N, b_int = d.z > N;
-        double qa[L][4], qb[L][4];
+        double qa[LCV][4], qb[LCV][4];
         double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
         int ha = 0, hb = 0;
         const double* Ta = tcp(st, 0);
         const double* Tb = tcp(st, 1);
 #pragma unroll
-        for (int j = 0; j < L; ++j) {
+        for (int j = 0; j < LCV; ++j) {
           double q[4], ea[4], eb[4];
           if (d.x == root) {
 #pragma unroll
@@ -402,7 +425,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
           }
           // outgoing pre-partials q_x = P_x^T top (engine.hpp:249-250)
           if (a_int) {
-            const double2* Tl = reinterpret_cast<const double2*>(Ta + j * NC * MP);
+            const double2* Tl = reinterpret_cast<const double2*>(Ta + (g * LCV + j) * NC * MP);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
@@ -411,7 +434,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
             }
           }
           if (b_int) {
-            const double2* Tl = reinterpret_cast<const double2*>(Tb + j * NC * MP);
+            const double2* Tl = reinterpret_cast<const double2*>(Tb + (g * LCV + j) * NC * MP);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
@@ -420,18 +443,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
             }
           }
         }
+        den = gsum(den);
+        na = gsum(na);
+        nb = gsum(nb);
+        if constexpr (HESS) {
+          na2 = gsum(na2);
+          nb2 = gsum(nb2);
+        }
+        ha = gmaxi(ha);
+        hb = gmaxi(hb);
         const double inv = 1.0 / den;
         {
           const double r1a = na * inv, r1b = nb * inv;
-          const double ga = warp_sum(valid ? w * r1a : 0.0);
-          const double gb = warp_sum(valid ? w * r1b : 0.0);
+          const double ga = warp_sum(owner ? w * r1a : 0.0);
+          const double gb = warp_sum(owner ? w * r1b : 0.0);
           if (lane == 0) {
             atomicAdd(A + d.y, ga);
             atomicAdd(A + d.z, gb);
           }
           if constexpr (HESS) {
-            const double ha2 = warp_sum(valid ? w * (na2 * inv - r1a * r1a) : 0.0);
-            const double hb2 = warp_sum(valid ? w * (nb2 * inv - r1b * r1b) : 0.0);
+            const double ha2 = warp_sum(owner ? w * (na2 * inv - r1a * r1a) : 0.0);
+            const double hb2 = warp_sum(owner ? w * (nb2 * inv - r1b * r1b) : 0.0);
             if (lane == 0) {
               atomicAdd(A + p.B + d.y, ha2);
               atomicAdd(A + p.B + d.z, hb2);
@@ -440,18 +472,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2) walk4_kernel(const __g
         }
         // normalise and hand on the pre-partials of internal children: the one
         // visited next stays in registers, the other goes to its scratch slot
-        auto emit = [&](const int x, double(&qx)[L][4], const int hx) {
+        auto emit = [&](const int x, double(&qx)[LCV][4], const int hx) {
           const int ex = peak_exponent(hx);
           const double scl = (ex != 0 && ex <= 1022) ? pow2_neg(ex) : 1.0;
           if (x == d.w) {
 #pragma unroll
-            for (int j = 0; j < L; ++j)
+            for (int j = 0; j < LCV; ++j)
 #pragma unroll
               for (int r = 0; r < 4; ++r) qreg[j][r] = qx[j][r] * scl;
           } else {
-            double2* dst = Qw + size_t(x) * 256;
+            double2* dst = Qw + size_t(x) * SD2;
 #pragma unroll
-            for (int j = 0; j < L; ++j) {
+            for (int j = 0; j < LCV; ++j) {
               __stcg(dst + (2 * j) * 32, make_double2(qx[j][0] * scl, qx[j][1] * scl));
               __stcg(dst + (2 * j + 1) * 32, make_double2(qx[j][2] * scl, qx[j][3] * scl));
             }
