@@ -488,7 +488,10 @@ struct pg_engine {
     walk_smem = 0;
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
-      walk4_lcv = 2;
+      // one lane per pattern unless that leaves fewer than ~2 tiles per
+      // resident warp slot (measured: C3 153 ms LCV=4 vs 180 ms LCV=2;
+      // C2 1.72 ms vs 1.55 ms)
+      walk4_lcv = (int64_t(P) / 32 >= int64_t(num_sms) * 8 * 2) ? 4 : 2;
       if (const char* v = std::getenv("PG_WALK4_LCV")) walk4_lcv = std::atoi(v) == 4 ? 4 : 2;
       G = 4 / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);
