@@ -26,6 +26,8 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv) {
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
 }
 int pg_walk4_nc(int nc);
+void* pg_walkm_kernel(int mp);
+size_t pg_walkm_smem(int mp);
 
 void* pg_walk_kernel_small(int MP, int LC);
 void* pg_walk_kernel_mid(int MP, int LC);
@@ -111,6 +113,8 @@ struct pg_engine {
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
+  bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
+  DevBuf<int> d_eexp, d_qexp;
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
   size_t walk_smem = 0;
   bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
@@ -471,7 +475,9 @@ struct pg_engine {
   int walk_max_blocks_per_sm();
 
   void prepare_geometry() {
-    MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
+    use_walkm = m > 8 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
+    if (use_walkm) MP = m <= 24 ? 24 : m <= 32 ? 32 : 64;
+    else MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
     int nc4 = 0;
     const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;
@@ -499,15 +505,32 @@ struct pg_engine {
       walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
                   sizeof(double2);
     }
+    if (use_walkm) {
+      use_walk4 = false;
+      LC = 1;
+      G = 4;  // a quad of lanes per pattern (DMMA fragment layout)
+      ntiles = (P + 31) / 32;  // CTA tiles of 32 patterns
+      walk_smem = pg_walkm_smem(MP);
+    }
     const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
-    const size_t vec = size_t(32) * LC * MP;
+    const size_t vec = use_walkm ? size_t(L) * 8 * MP : size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
     size_t free_b = 0, total_b = 0;
     PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t budget = size_t(double(free_b) * 0.6);
     int cap = int(std::max<size_t>(1, budget / per_warp));
-    TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
-    TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
+    if (use_walkm) {
+      // CTA tiles: 4 warps per tile
+      int ctas = std::max(1, std::min({maxw / 4, std::max(ntiles, 1), std::max(cap / 4, 1)}));
+      TW = ctas * 4;
+    } else {
+      TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
+      TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
+    }
+    if (use_walkm) {
+      d_eexp.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * L * 8);
+      d_qexp.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * L * 8);
+    }
     accw = 1 + 2 * B();
     d_escr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
     d_qscr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
@@ -666,6 +689,12 @@ void* select_walk(int MP, int LC) {
 
 int pg_engine::walk_max_blocks_per_sm() {
   int nb = 0;
+  if (use_walkm) {
+    const void* fn = pg_walkm_kernel(MP);
+    PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, walk_smem));
+    return std::max(nb, 1);
+  }
   if (use_walk4) {
     // occupancy of the heaviest variant (per-branch Q + Hessian) bounds the grid
     for (int v = 0; v < 4; ++v) {
@@ -745,6 +774,16 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   p.disable = opt.disable_rescaling;
   p.do_pre = do_pre ? 1 : 0;
   p.hess = do_hess ? 1 : 0;
+  if (use_walkm) {
+    pgk::WalkMParams pm{};
+    pm.p = p;
+    pm.eexp = d_eexp.p;
+    pm.qexp = d_qexp.p;
+    void* fn = pg_walkm_kernel(MP);
+    void* args[] = {&pm};
+    PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / 4)), dim3(128), args, walk_smem, stream));
+    return;
+  }
   if (use_walk4) {
     pgk::Walk4Params p4{};
     p4.p = p;
@@ -987,7 +1026,7 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
   });
 }
 
-int pg_engine_variant(const pg_engine* e) { return e->use_walk4 ? 1 : 0; }
+int pg_engine_variant(const pg_engine* e) { return e->use_walkm ? 2 : e->use_walk4 ? 1 : 0; }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {
   return guarded([&] {

@@ -63,6 +63,13 @@ struct Walk4Params {
   double pi[4];
 };
 
+// Parameters of the DMMA large-state kernel (pg_walkm.cuh).
+struct WalkMParams {
+  WalkParams p;
+  int* eexp;  // [TW][N-1][L][8] exponents of the stored edge messages
+  int* qexp;  // [TW][N-1][L][8] exponents of the stored pre-partials
+};
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

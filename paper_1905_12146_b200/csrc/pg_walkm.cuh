@@ -1,0 +1,374 @@
+// K2 for large state spaces (m = 9..64: amino acids, codons) on the fp64
+// tensor cores (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind).
+//
+// Work unit: a CTA of 4 warps owns 32 patterns (8 per warp) and walks the
+// tree in lock-step, one (node, rate category) at a time, so each P(t) block
+// (MP x MP fp64) is staged once in shared memory and reused by all 32
+// patterns.  Every mat-vec  y^T = x^T M  over a warp's 8 patterns is a chain of
+// DMMA tiles: A = x^T (8 patterns x 4 states), B = 4 x 8 slice of M, D = y^T
+// (8 patterns x 8 states).  Vectors live in the A-fragment layout (pattern =
+// lane/4, states 4k + lane%4); the D fragments are converted back through a
+// per-warp shared buffer.
+//
+// Scaling: categories are processed one at a time, so each (pattern,
+// category) vector carries its own power-of-two exponent (stored beside the
+// scratch slots); mixtures over categories (root likelihood, gradient
+// numerator/denominator) are combined with those exponents.  Post partials are
+// normalised per category at every node (exact), pre partials when produced.
+#pragma once
+
+#include "pg_walk.cuh"
+
+namespace pgk {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
+template <int MP>
+struct WalkMGeom {
+  static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
+  static constexpr int NT = MP / 8;  // n-tiles (D fragments per vector per lane)
+  // padded smem row stride (doubles): S % 16 == 4 makes both B-fragment access
+  // patterns (row-major and column-major reads) bank-conflict free
+  static constexpr int S = ((MP + 4) % 16 == 4) ? MP + 4 : MP + 12;
+  static constexpr int CONV = 8 * S;  // per-warp conversion buffer (doubles)
+  static constexpr size_t smem_bytes() { return size_t(2 * MP * S + 4 * CONV) * sizeof(double); }
+};
+
+template <int MP>
+__global__ void __launch_bounds__(128, 2) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+  using Gm = WalkMGeom<MP>;
+  constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
+  const WalkParams& p = PM.p;
+  extern __shared__ __align__(16) double smd[];
+  double* Pbuf0 = smd;
+  double* Pbuf1 = smd + MP * S;
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  double* conv = smd + 2 * MP * S + wib * Gm::CONV;
+  const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
+  const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
+  const int warp = blockIdx.x * 4 + wib;
+  const int ntile_cta = (p.P + 31) / 32;
+  const size_t slotd = size_t(L) * K * 32;  // doubles per node slot per warp
+  double* E = p.escr + size_t(warp) * size_t(N - 1) * slotd;
+  double* Qs = p.qscr + size_t(warp) * size_t(N - 1) * slotd;
+  int* Ex = PM.eexp + size_t(warp) * size_t(N - 1) * L * 8;
+  int* Qx = PM.qexp + size_t(warp) * size_t(N - 1) * L * 8;
+  double* Acc = p.acc + size_t(warp) * p.accw;
+  for (int i = lane; i < p.accw; i += 32) Acc[i] = 0.0;
+  __syncwarp();
+
+  // stage the first MP columns (post: P) of one (node, category) TC block,
+  // rows padded to stride S; element (row r, col c) of P at buf[c * S + r]
+  auto stage_P = [&](double* buf, int node, int l) {
+    const double* src = p.tc + (size_t(node - 1) * L + l) * size_t(NC) * MP;
+    constexpr int CH = MP / 2;  // 16 B chunks per column
+    for (int i = tid; i < MP * CH; i += 128) {
+      const int c = i / CH, h = i % CH;
+      cpa16(buf + c * S + 2 * h, src + c * MP + 2 * h);
+    }
+  };
+  // x (A layout) -> y = M x through DMMA; B element (k, n) = Msm(k, n) given by fn
+  auto convert_store = [&](double (&d)[NT][2], double (&y)[K]) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      conv[q * S + ni * 8 + 2 * t] = d[ni][0];
+      conv[q * S + ni * 8 + 2 * t + 1] = d[ni][1];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ki = 0; ki < K; ++ki) y[ki] = conv[q * S + ki * 4 + t];
+    __syncwarp();
+  };
+  // e = P x with P staged column-major (TC columns): B(k, n) = P[n][k] = buf[k * S + n]
+  auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      d[ni][0] = d[ni][1] = 0.0;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], buf[(ki * 4 + t) * S + ni * 8 + q]);
+    }
+    convert_store(d, y);
+  };
+  // y = P^T x: B(k, n) = P[k][n] = buf[n * S + k]
+  auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      d[ni][0] = d[ni][1] = 0.0;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], buf[(ni * 8 + q) * S + ki * 4 + t]);
+    }
+    convert_store(d, y);
+  };
+  // y = Q x with Q row-major in global (L1-resident): B(k, n) = Q[n][k]
+  auto matvec_Q = [&](const double* Qm, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      d[ni][0] = d[ni][1] = 0.0;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t));
+    }
+    convert_store(d, y);
+  };
+  auto quad_sum = [&](double v) {
+    v += __shfl_xor_sync(kFull, v, 1);
+    v += __shfl_xor_sync(kFull, v, 2);
+    return v;
+  };
+  // exponent of the per-pattern peak (quad reduction) of K non-negative values
+  auto quad_peak_exp = [&](const double (&v)[K]) {
+    int h = 0;
+#pragma unroll
+    for (int ki = 0; ki < K; ++ki) h = max(h, __double2hiint(v[ki]));
+    h = max(h, __shfl_xor_sync(kFull, h, 1));
+    h = max(h, __shfl_xor_sync(kFull, h, 2));
+    const int bexp = (h >> 20) & 0x7ff;
+    if (h <= 0 || bexp == 0x7ff || bexp == 0) return 0;
+    return bexp - 1022;
+  };
+  auto scale_by = [&](double (&v)[K], int ex) {
+    if (ex == 0) return;
+    if (ex > -1021 && ex < 1022) {
+      const double sc = __hiloint2double((1023 - ex) << 20, 0);
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] *= sc;
+    } else {
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] = ldexp(v[ki], -ex);
+    }
+  };
+  // running mixture over categories with exponents: value = acc * 2^ref
+  struct Mix {
+    double v[5];
+    int ref;
+  };
+
+  for (int tile = blockIdx.x; tile < ntile_cta; tile += gridDim.x) {
+    const int s = tile * 32 + wib * 8 + q;
+    const bool valid = s < p.P;
+    const bool owner = valid && t == 0;
+    const int sc = valid ? s : p.P - 1;
+    const double w = valid ? p.weights[sc] : 0.0;
+    const uint8_t* codes = p.codes + sc;
+    const size_t Pc = size_t(p.Pc);
+
+    auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
+      const double* src = base + size_t(node - N - 1) * slotd + size_t(l) * K * 32 + lane;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] = __ldcg(src + ki * 32);
+    };
+    auto store_slot = [&](double* base, int node, int l, const double (&v)[K]) {
+      double* dst = base + size_t(node - N - 1) * slotd + size_t(l) * K * 32 + lane;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) __stcg(dst + ki * 32, v[ki]);
+    };
+    auto gather = [&](int node, int code, int l, double (&v)[K]) {
+      const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
+    };
+    auto exp_idx = [&](int node, int l) { return (size_t(node - N - 1) * L + l) * 8 + q; };
+
+    // ------------------------------------------------ post-order pass (a)
+    for (int i = 0; i < p.nsteps; ++i) {
+      const int4 st = p.post[i];
+      const int k = st.x;
+      const int code0 = st.y <= N ? codes[size_t(st.y - 1) * Pc] : 0;
+      const int code1 = st.z <= N ? codes[size_t(st.z - 1) * Pc] : 0;
+      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      for (int l = 0; l < L; ++l) {
+        __syncthreads();
+        if (k != root) stage_P(Pbuf0, k, l);
+        double a[K], b[K];
+        int xa = 0, xb = 0;
+        if (st.y <= N) gather(st.y, code0, l, a);
+        else {
+          load_slot(E, st.y, l, a);
+          xa = Ex[exp_idx(st.y, l)];
+        }
+        if (st.z <= N) gather(st.z, code1, l, b);
+        else {
+          load_slot(E, st.z, l, b);
+          xb = Ex[exp_idx(st.z, l)];
+        }
+#pragma unroll
+        for (int ki = 0; ki < K; ++ki) a[ki] *= b[ki];
+        int ex = p.disable ? 0 : quad_peak_exp(a);
+        scale_by(a, ex);
+        const int Sk = xa + xb + ex;
+        if (k == root) {
+          double d = 0.0;
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) d = fma(p.pi[ki * 4 + t], a[ki], d);
+          d = quad_sum(d) * p.probs[l];
+          // combine with the running mixture (rebased to the larger exponent)
+          if (Sk > mix.ref) {
+            mix.v[0] = mix.ref == INT_MIN ? 0.0 : ldexp(mix.v[0], mix.ref - Sk);
+            mix.ref = Sk;
+          }
+          mix.v[0] += ldexp(d, Sk - mix.ref);
+        } else {
+          cpa_commit_wait_all();
+          __syncthreads();
+          double e[K];
+          matvec_P(Pbuf0, a, e);
+          store_slot(E, k, l, e);
+          if (t == 0) Ex[exp_idx(k, l)] = Sk;
+        }
+      }
+      if (k == root) {
+        const double m = mix.v[0];
+        const double ll = log(m) + double(mix.ref) * 0.6931471805599453;
+        if (owner) {
+          if (!isfinite(m)) atomicMin(&p.err[0], s);
+          else if (m <= 0.0) atomicMin(&p.err[1], s);
+          if (p.site_ll) p.site_ll[s] = ll;
+        }
+        const double v = warp_sum(owner ? w * ll : 0.0);
+        if (lane == 0) atomicAdd(Acc, v);
+      }
+    }
+    if (!p.do_pre) continue;
+
+    // ----------------------------------- pre-order pass + gradient (b)+(c)
+    for (int i = 0; i < p.nsteps; ++i) {
+      const int4 st = p.pre[i];
+      const int k = st.x, ca = st.y, cb = st.z;
+      const bool a_int = ca > N, b_int = cb > N;
+      const int code0 = !a_int ? codes[size_t(ca - 1) * Pc] : 0;
+      const int code1 = !b_int ? codes[size_t(cb - 1) * Pc] : 0;
+      const double* Qa = p.qtab + size_t(p.qidx[ca]) * MP * MP;
+      const double* Qb = p.qtab + size_t(p.qidx[cb]) * MP * MP;
+      // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
+      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      for (int l = 0; l < L; ++l) {
+        __syncthreads();
+        if (a_int) stage_P(Pbuf0, ca, l);
+        if (b_int) stage_P(Pbuf1, cb, l);
+        double qv[K], ea[K], eb[K];
+        int xq = 0, xa = 0, xb = 0;
+        if (k == root) {
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
+        } else {
+          load_slot(Qs, k, l, qv);
+          xq = Qx[exp_idx(k, l)];
+        }
+        if (a_int) {
+          load_slot(E, ca, l, ea);
+          xa = Ex[exp_idx(ca, l)];
+        } else gather(ca, code0, l, ea);
+        if (b_int) {
+          load_slot(E, cb, l, eb);
+          xb = Ex[exp_idx(cb, l)];
+        } else gather(cb, code1, l, eb);
+        const int El = xq + xa + xb;
+        double ta[K], tb[K], dd = 0.0;
+#pragma unroll
+        for (int ki = 0; ki < K; ++ki) {
+          ta[ki] = qv[ki] * eb[ki];
+          tb[ki] = qv[ki] * ea[ki];
+          dd = fma(ta[ki], ea[ki], dd);
+        }
+        const double wl = p.probs[l], cl = p.rates[l];
+        double term[5];
+        term[0] = wl * quad_sum(dd);
+        {
+          double u[K];
+          matvec_Q(Qa, ea, u);
+          double d1 = 0.0;
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) d1 = fma(ta[ki], u[ki], d1);
+          term[1] = cl * wl * quad_sum(d1);
+          if (p.hess) {
+            double u2[K];
+            matvec_Q(Qa, u, u2);
+            double d2 = 0.0;
+#pragma unroll
+            for (int ki = 0; ki < K; ++ki) d2 = fma(ta[ki], u2[ki], d2);
+            term[3] = cl * cl * wl * quad_sum(d2);
+          } else {
+            term[3] = 0.0;
+          }
+        }
+        {
+          double u[K];
+          matvec_Q(Qb, eb, u);
+          double d1 = 0.0;
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) d1 = fma(tb[ki], u[ki], d1);
+          term[2] = cl * wl * quad_sum(d1);
+          if (p.hess) {
+            double u2[K];
+            matvec_Q(Qb, u, u2);
+            double d2 = 0.0;
+#pragma unroll
+            for (int ki = 0; ki < K; ++ki) d2 = fma(tb[ki], u2[ki], d2);
+            term[4] = cl * cl * wl * quad_sum(d2);
+          } else {
+            term[4] = 0.0;
+          }
+        }
+        if (El > mix.ref) {
+          if (mix.ref != INT_MIN)
+            for (int r = 0; r < 5; ++r) mix.v[r] = ldexp(mix.v[r], mix.ref - El);
+          mix.ref = El;
+        }
+        const double sc = ldexp(1.0, El - mix.ref);
+        for (int r = 0; r < 5; ++r) mix.v[r] = fma(term[r], sc, mix.v[r]);
+        // outgoing pre-partials of internal children: q_x = P_x^T top
+        if (a_int || b_int) {
+          cpa_commit_wait_all();
+          __syncthreads();
+        }
+        if (a_int) {
+          double qo[K];
+          matvec_PT(Pbuf0, ta, qo);
+          const int ex = quad_peak_exp(qo);
+          scale_by(qo, ex);
+          store_slot(Qs, ca, l, qo);
+          if (t == 0) Qx[exp_idx(ca, l)] = xq + xb + ex;
+        }
+        if (b_int) {
+          double qo[K];
+          matvec_PT(Pbuf1, tb, qo);
+          const int ex = quad_peak_exp(qo);
+          scale_by(qo, ex);
+          store_slot(Qs, cb, l, qo);
+          if (t == 0) Qx[exp_idx(cb, l)] = xq + xa + ex;
+        }
+      }
+      const double inv = 1.0 / mix.v[0];
+      const double r1a = mix.v[1] * inv, r1b = mix.v[2] * inv;
+      const double ga = warp_sum(owner ? w * r1a : 0.0);
+      const double gb = warp_sum(owner ? w * r1b : 0.0);
+      if (lane == 0) {
+        atomicAdd(Acc + ca, ga);
+        atomicAdd(Acc + cb, gb);
+      }
+      if (p.hess) {
+        const double ha = warp_sum(owner ? w * (mix.v[3] * inv - r1a * r1a) : 0.0);
+        const double hb = warp_sum(owner ? w * (mix.v[4] * inv - r1b * r1b) : 0.0);
+        if (lane == 0) {
+          atomicAdd(Acc + p.B + ca, ha);
+          atomicAdd(Acc + p.B + cb, hb);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace pgk
