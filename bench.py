@@ -79,6 +79,20 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def fp64_tensor_peak():
+    """DMMA (mma.sync m8n8k4 f64) peak measured on this pool's B200 by
+    scripts/fp64_peak.cu (profiles/fp64_peak_b200.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_b200.json")) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("kernel", "").startswith("dmma"):
+                    return float(d["tflops"]), "measured (scripts/fp64_peak.cu)"
+    except Exception:
+        pass
+    return 37.0, "fallback (datasheet)"
+
+
 def profiled_traffic(config):
     """DRAM bytes per walk launch from the committed ncu capture, if any."""
     try:
@@ -341,10 +355,23 @@ def main():
     e2e_s = float(te[0])
 
     if rank == 0:
-        peak, peak_kind = measured_peaks()
-        balg = bytes_alg(inst, p1 - p0)
-        achieved = balg / (walk_ms_max * 1e-3) / 1e9
         prof = profiled_traffic(args.config)
+        if inst.states > 32:
+            # codon path: fp64 tensor-core bound (AI = 9.2 flop/B)
+            peak, peak_kind = fp64_tensor_peak()
+            falg = flops_alg(inst, p1 - p0)
+            achieved = falg / (walk_ms_max * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "peak_source": peak_kind, "algorithmic_flops_per_launch": falg}
+        else:
+            peak, peak_kind = measured_peaks()
+            balg = bytes_alg(inst, p1 - p0)
+            achieved = balg / (walk_ms_max * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": balg}
+        roof.update({"kernel": eng.info()["kernel"] + " (post + pre + fused gradient)", "walk_ms": walk_ms_max,
+                     "traffic": prof["dram_bytes_per_launch"] if prof else None,
+                     "traffic_source": prof.get("source") if prof else None})
         value = P_total * B / (ms * 1e-3)
         info = eng.info()
         line = {
@@ -359,12 +386,7 @@ def main():
                        "parallelism": f"pattern-shard dp{world}",
                        "l2": "inputs larger than L2 (edge scratch + tip codes >> 126 MB); no flush",
                        "setup_s": round(t_gen, 2), "geometry": info},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_source": peak_kind,
-                         "kernel": "walk_kernel (post+pre+gradient)",
-                         "algorithmic_bytes_per_launch": balg, "walk_ms": walk_ms_max,
-                         "traffic": prof["dram_bytes_per_launch"] if prof else None,
-                         "traffic_source": prof["source"] if prof else None},
+            "roofline": roof,
             "e2e": {"value": P_total * B / e2e_s, "unit": "pattern-branch/s", "ms_per_step": e2e_s * 1e3,
                     "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": 8 * (1 + B)},
             "gpu_launches": info["launches"] * args.steps,
