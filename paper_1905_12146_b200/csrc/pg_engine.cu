@@ -779,6 +779,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     pm.p = p;
     pm.eexp = d_eexp.p;
     pm.qexp = d_qexp.p;
+    pm.homogeneous = branch_q.empty() ? 1 : 0;
     void* fn = pg_walkm_kernel(MP);
     void* args[] = {&pm};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / 4)), dim3(128), args, walk_smem, stream));

@@ -68,6 +68,7 @@ struct WalkMParams {
   WalkParams p;
   int* eexp;  // [TW][N-1][L][8] exponents of the stored edge messages
   int* qexp;  // [TW][N-1][L][8] exponents of the stored pre-partials
+  int homogeneous;  // stage the shared generator in shared memory
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -41,20 +41,20 @@ struct WalkMGeom {
   // padded smem row stride (doubles): S % 16 == 4 makes both B-fragment access
   // patterns (row-major and column-major reads) bank-conflict free
   static constexpr int S = ((MP + 4) % 16 == 4) ? MP + 4 : MP + 12;
-  static constexpr int CONV = 8 * S;  // per-warp conversion buffer (doubles)
-  static constexpr size_t smem_bytes() { return size_t(2 * MP * S + 4 * CONV) * sizeof(double); }
+  // two P(t) blocks (the children of a pre-order step) + the generator Q
+  static constexpr size_t smem_bytes() { return size_t(3 * MP * S) * sizeof(double); }
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, 2) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
   const WalkParams& p = PM.p;
   extern __shared__ __align__(16) double smd[];
   double* Pbuf0 = smd;
   double* Pbuf1 = smd + MP * S;
+  double* Qsm = smd + 2 * MP * S;  // homogeneous generator, row-major, stride S
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  double* conv = smd + 2 * MP * S + wib * Gm::CONV;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
   const int warp = blockIdx.x * 4 + wib;
@@ -78,48 +78,59 @@ __global__ void __launch_bounds__(128, 2) walkm_kernel(const __grid_constant__ W
       cpa16(buf + c * S + 2 * h, src + c * MP + 2 * h);
     }
   };
-  // x (A layout) -> y = M x through DMMA; B element (k, n) = Msm(k, n) given by fn
+  // D fragments (lane (q,t) holds states 8ni + 2t, 8ni + 2t + 1) -> A layout
+  // (lane (q,t) holds states 4ki + t): state 8ni + 4h + t lives in lane
+  // 4q + 2h + t/2, element t%2 — two shuffles per k-step, no shared memory.
   auto convert_store = [&](double (&d)[NT][2], double (&y)[K]) {
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      conv[q * S + ni * 8 + 2 * t] = d[ni][0];
-      conv[q * S + ni * 8 + 2 * t + 1] = d[ni][1];
+    for (int ki = 0; ki < K; ++ki) {
+      const int ni = ki >> 1, h = ki & 1;
+      const int src = (q << 2) + 2 * h + (t >> 1);
+      const double v0 = __shfl_sync(kFull, d[ni][0], src);
+      const double v1 = __shfl_sync(kFull, d[ni][1], src);
+      y[ki] = (t & 1) ? v1 : v0;
     }
-    __syncwarp();
-#pragma unroll
-    for (int ki = 0; ki < K; ++ki) y[ki] = conv[q * S + ki * 4 + t];
-    __syncwarp();
   };
   // e = P x with P staged column-major (TC columns): B(k, n) = P[n][k] = buf[k * S + n]
   auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      d[ni][0] = d[ni][1] = 0.0;
+    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], buf[(ki * 4 + t) * S + ni * 8 + q]);
-    }
+    for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], buf[(ki * 4 + t) * S + ni * 8 + q]);
     convert_store(d, y);
   };
   // y = P^T x: B(k, n) = P[k][n] = buf[n * S + k]
   auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      d[ni][0] = d[ni][1] = 0.0;
+    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], buf[(ni * 8 + q) * S + ki * 4 + t]);
-    }
+    for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], buf[(ni * 8 + q) * S + ki * 4 + t]);
     convert_store(d, y);
   };
-  // y = Q x with Q row-major in global (L1-resident): B(k, n) = Q[n][k]
+  // y = Q x: homogeneous Q staged row-major in smem (B(k, n) = Q[n][k] =
+  // Qsm[n * S + k]); per-branch generators read from global (L1-resident)
+  const bool homog = PM.homogeneous != 0;
   auto matvec_Q = [&](const double* Qm, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      d[ni][0] = d[ni][1] = 0.0;
+    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
+    if (homog) {
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) dmma(d[ni][0], d[ni][1], x[ki], __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t));
+      for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], Qsm[(ni * 8 + q) * S + ki * 4 + t]);
+    } else {
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+          dmma(d[ni][0], d[ni][1], x[ki], __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t));
     }
     convert_store(d, y);
   };
@@ -155,6 +166,11 @@ __global__ void __launch_bounds__(128, 2) walkm_kernel(const __grid_constant__ W
     double v[5];
     int ref;
   };
+
+  if (homog) {
+    for (int i = tid; i < MP * MP; i += 128) Qsm[(i / MP) * S + (i % MP)] = p.qtab[i];
+    __syncthreads();
+  }
 
   for (int tile = blockIdx.x; tile < ntile_cta; tile += gridDim.x) {
     const int s = tile * 32 + wib * 8 + q;
