@@ -121,6 +121,7 @@ struct pg_engine {
 
   // device state
   DevBuf<uint8_t> d_codes;
+  DevBuf<double> d_qtc;
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err;
   DevBuf<int4> d_post, d_pre;
@@ -539,6 +540,7 @@ struct pg_engine {
     d_site_ll.ensure(size_t(std::max(P, 1)));
     d_err.ensure(3);
     d_tc.ensure(size_t(B()) * L * NC * MP);
+    if (use_walkm) d_qtc.ensure(size_t(B()) * L * NC * MP);
     d_post.upload(post_steps.data(), post_steps.size(), stream);
     d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
     if (!h_out) {
@@ -721,6 +723,7 @@ void pg_engine::launch_tc() {
   p.eig_w = d_ew.p;
   p.amb = d_amb.p;
   p.tc = d_tc.p;
+  p.qtc = use_walkm ? d_qtc.p : nullptr;
   p.err = d_err.p;
   p.m = m;
   p.MP = MP;
@@ -741,6 +744,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   p.codes = d_codes.p;
   p.weights = d_weights.p;
   p.tc = d_tc.p;
+  p.qtc = use_walkm ? d_qtc.p : nullptr;
   p.qtab = d_qtab.p;
   p.qidx = d_qidx.p;
   p.pi = d_pi.p;

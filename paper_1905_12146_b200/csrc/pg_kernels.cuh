@@ -41,6 +41,7 @@ struct TcParams {
   const double* eig_w;  // [m] eigenvalues
   const double* amb;    // [A][m] ambiguity partials
   double* tc;           // [B][L][NC][MP]
+  double* qtc;          // optional [B][L][NC][MP]: the same columns of Q_branch * P (tip Q-e gathers)
   int* err;             // err[2] <- 1 on a negative / non-finite branch length
   int m, MP, NC, A, L, have_eigen;
 };
@@ -232,6 +233,33 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
       }
     }
     out[e] = v;
+  }
+  if (p.qtc) {
+    // Q e for a tip is a column of Q P (P and Q commute, engine.hpp:260):
+    // build QR = Q_branch * R once, then the same column table
+    double* QR = sm + 5 * mm;  // dead expm buffer, disjoint from R
+    const double* Q = p.qtab + size_t(qi) * p.MP * p.MP;
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) {
+      const int i = e / m, j = e % m;
+      double s = 0.0;
+      for (int k = 0; k < m; ++k) s = fma(Q[i * p.MP + k], R[k * m + j], s);
+      QR[e] = s;
+    }
+    __syncthreads();
+    double* qout = p.qtc + (size_t(node - 1) * p.L + l) * p.NC * p.MP;
+    for (int e = threadIdx.x; e < p.NC * p.MP; e += blockDim.x) {
+      const int c = e / p.MP, r = e % p.MP;
+      double v = 0.0;
+      if (r < m) {
+        if (c < p.MP) {
+          if (c < m) v = QR[r * m + c];
+        } else if (c - p.MP < p.A) {
+          const double* a = p.amb + size_t(c - p.MP) * m;
+          for (int j = 0; j < m; ++j) v = fma(QR[r * m + j], a[j], v);
+        }
+      }
+      qout[e] = v;
+    }
   }
 }
 

@@ -34,6 +34,7 @@ struct WalkParams {
   const uint8_t* codes;  // [N][Pc] tip column index into the TC table (rows padded to 32)
   const double* weights; // [P]
   const double* tc;      // [B][L][NC][MP]: column c of P (c < MP) or P*ambiguity (c >= MP)
+  const double* qtc;     // same table for Q*P (walkm tips), may be null
   const double* qtab;    // [nq][MP][MP] row-major generators
   const int* qidx;       // [2N] node -> generator index
   const double* pi;      // [MP]

@@ -161,6 +161,11 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       for (int ki = 0; ki < K; ++ki) v[ki] = ldexp(v[ki], -ex);
     }
   };
+  // 2^e for e <= 0 (exact down to the subnormal range; 0 below)
+  auto pow2 = [](int e) -> double {
+    if (e >= -1022) return __hiloint2double((1023 + e) << 20, 0);
+    return e >= -1074 ? ldexp(1.0, e) : 0.0;
+  };
   // running mixture over categories with exponents: value = acc * 2^ref
   struct Mix {
     double v[5];
@@ -193,6 +198,12 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
       const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
+    };
+    // Q e of a tip = the same column of Q P (built by K1): a gather, not a mat-vec
+    auto gather_q = [&](int node, int code, int l, double (&v)[K]) {
+      const double* col = p.qtc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
 #pragma unroll
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
@@ -232,10 +243,10 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
           d = quad_sum(d) * p.probs[l];
           // combine with the running mixture (rebased to the larger exponent)
           if (Sk > mix.ref) {
-            mix.v[0] = mix.ref == INT_MIN ? 0.0 : ldexp(mix.v[0], mix.ref - Sk);
+            mix.v[0] = mix.ref == INT_MIN ? 0.0 : mix.v[0] * pow2(mix.ref - Sk);
             mix.ref = Sk;
           }
-          mix.v[0] += ldexp(d, Sk - mix.ref);
+          mix.v[0] += d * pow2(Sk - mix.ref);
         } else {
           cpa_commit_wait_all();
           __syncthreads();
@@ -304,7 +315,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         term[0] = wl * quad_sum(dd);
         {
           double u[K];
-          matvec_Q(Qa, ea, u);
+          if (a_int) matvec_Q(Qa, ea, u);
+          else gather_q(ca, code0, l, u);
           double d1 = 0.0;
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) d1 = fma(ta[ki], u[ki], d1);
@@ -322,7 +334,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         }
         {
           double u[K];
-          matvec_Q(Qb, eb, u);
+          if (b_int) matvec_Q(Qb, eb, u);
+          else gather_q(cb, code1, l, u);
           double d1 = 0.0;
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) d1 = fma(tb[ki], u[ki], d1);
@@ -339,11 +352,13 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
           }
         }
         if (El > mix.ref) {
-          if (mix.ref != INT_MIN)
-            for (int r = 0; r < 5; ++r) mix.v[r] = ldexp(mix.v[r], mix.ref - El);
+          if (mix.ref != INT_MIN) {
+            const double down = pow2(mix.ref - El);
+            for (int r = 0; r < 5; ++r) mix.v[r] *= down;
+          }
           mix.ref = El;
         }
-        const double sc = ldexp(1.0, El - mix.ref);
+        const double sc = pow2(El - mix.ref);
         for (int r = 0; r < 5; ++r) mix.v[r] = fma(term[r], sc, mix.v[r]);
         // outgoing pre-partials of internal children: q_x = P_x^T top
         if (a_int || b_int) {
