@@ -46,9 +46,10 @@ struct WalkMGeom {
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
+  constexpr bool PF = MP <= 32;  // register budget allows cross-category operand prefetch
   const WalkParams& p = PM.p;
   extern __shared__ __align__(16) double smd[];
   double* Pbuf0 = smd;
@@ -216,11 +217,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       const int code0 = st.y <= N ? codes[size_t(st.y - 1) * Pc] : 0;
       const int code1 = st.z <= N ? codes[size_t(st.z - 1) * Pc] : 0;
       Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
-      for (int l = 0; l < L; ++l) {
-        __syncthreads();
-        if (k != root) stage_P(Pbuf0, k, l);
-        double a[K], b[K];
-        int xa = 0, xb = 0;
+      auto load_post = [&](int l, double (&a)[K], double (&b)[K], int& xa, int& xb) {
+        xa = xb = 0;
         if (st.y <= N) gather(st.y, code0, l, a);
         else {
           load_slot(E, st.y, l, a);
@@ -230,6 +228,29 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         else {
           load_slot(E, st.z, l, b);
           xb = Ex[exp_idx(st.z, l)];
+        }
+      };
+      // small state spaces: the next category's operands are loaded while
+      // this category computes (software pipeline over categories)
+      double an[K], bn[K];
+      int xan = 0, xbn = 0;
+      if constexpr (PF) load_post(0, an, bn, xan, xbn);
+      for (int l = 0; l < L; ++l) {
+        __syncthreads();
+        if (k != root) stage_P(Pbuf0, k, l);
+        double a[K], b[K];
+        int xa = 0, xb = 0;
+        if constexpr (PF) {
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) {
+            a[ki] = an[ki];
+            b[ki] = bn[ki];
+          }
+          xa = xan;
+          xb = xbn;
+          if (l + 1 < L) load_post(l + 1, an, bn, xan, xbn);
+        } else {
+          load_post(l, a, b, xa, xb);
         }
 #pragma unroll
         for (int ki = 0; ki < K; ++ki) a[ki] *= b[ki];
@@ -281,12 +302,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       const double* Qb = p.qtab + size_t(p.qidx[cb]) * MP * MP;
       // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
       Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
-      for (int l = 0; l < L; ++l) {
-        __syncthreads();
-        if (a_int) stage_P(Pbuf0, ca, l);
-        if (b_int) stage_P(Pbuf1, cb, l);
-        double qv[K], ea[K], eb[K];
-        int xq = 0, xa = 0, xb = 0;
+      auto load_pre = [&](int l, double (&qv)[K], double (&ea)[K], double (&eb)[K], int& xq, int& xa, int& xb) {
+        xq = xa = xb = 0;
         if (k == root) {
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
@@ -302,6 +319,30 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
           load_slot(E, cb, l, eb);
           xb = Ex[exp_idx(cb, l)];
         } else gather(cb, code1, l, eb);
+      };
+      double qn[K], ean[K], ebn[K];
+      int xqn = 0, xan = 0, xbn = 0;
+      if constexpr (PF) load_pre(0, qn, ean, ebn, xqn, xan, xbn);
+      for (int l = 0; l < L; ++l) {
+        __syncthreads();
+        if (a_int) stage_P(Pbuf0, ca, l);
+        if (b_int) stage_P(Pbuf1, cb, l);
+        double qv[K], ea[K], eb[K];
+        int xq = 0, xa = 0, xb = 0;
+        if constexpr (PF) {
+#pragma unroll
+          for (int ki = 0; ki < K; ++ki) {
+            qv[ki] = qn[ki];
+            ea[ki] = ean[ki];
+            eb[ki] = ebn[ki];
+          }
+          xq = xqn;
+          xa = xan;
+          xb = xbn;
+          if (l + 1 < L) load_pre(l + 1, qn, ean, ebn, xqn, xan, xbn);
+        } else {
+          load_pre(l, qv, ea, eb, xq, xa, xb);
+        }
         const int El = xq + xa + xb;
         double ta[K], tb[K], dd = 0.0;
 #pragma unroll
