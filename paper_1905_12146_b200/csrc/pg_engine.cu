@@ -575,6 +575,9 @@ struct pg_engine {
   void enqueue(int flags, double* out_device) {
     check_ready();
     set_device();
+    // a forced evaluation rebuilds P(t) like the reference's post pass, which
+    // recomputes trans_ every time (engine.hpp:197-201)
+    if (flags & PG_EVAL_FORCE) tc_dirty = true;
     if (geometry_dirty) prepare_geometry();
     if (model_dirty) upload_model();
     const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);

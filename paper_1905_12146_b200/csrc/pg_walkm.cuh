@@ -46,10 +46,12 @@ struct WalkMGeom {
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
-  constexpr bool PF = MP <= 32;  // register budget allows cross-category operand prefetch
+  // cross-category operand prefetch: measured slower on C4 (266 vs 236 ms) because
+  // the extra registers cost a resident CTA; kept selectable
+  constexpr bool PF = false;
   const WalkParams& p = PM.p;
   extern __shared__ __align__(16) double smd[];
   double* Pbuf0 = smd;
@@ -209,11 +211,23 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
     auto exp_idx = [&](int node, int l) { return (size_t(node - N - 1) * L + l) * 8 + q; };
+    // bring a whole node slot (all categories) of this warp into L2 ahead of use
+    auto prefetch_slot = [&](const double* base, int node) {
+      if (node <= N) return;
+      const char* b = reinterpret_cast<const char*>(base + size_t(node - N - 1) * slotd);
+      const int lines = int(slotd * 8 / 128);
+      for (int i = lane; i < lines; i += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + size_t(i) * 128));
+    };
 
     // ------------------------------------------------ post-order pass (a)
     for (int i = 0; i < p.nsteps; ++i) {
       const int4 st = p.post[i];
       const int k = st.x;
+      if (i + 1 < p.nsteps) {  // next step's stored operands -> L2 while this step computes
+        const int4 nx = p.post[i + 1];
+        prefetch_slot(E, nx.y);
+        prefetch_slot(E, nx.z);
+      }
       const int code0 = st.y <= N ? codes[size_t(st.y - 1) * Pc] : 0;
       const int code1 = st.z <= N ? codes[size_t(st.z - 1) * Pc] : 0;
       Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
@@ -295,6 +309,12 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
     for (int i = 0; i < p.nsteps; ++i) {
       const int4 st = p.pre[i];
       const int k = st.x, ca = st.y, cb = st.z;
+      if (i + 1 < p.nsteps) {
+        const int4 nx = p.pre[i + 1];
+        if (nx.x != root) prefetch_slot(Qs, nx.x);
+        prefetch_slot(E, nx.y);
+        prefetch_slot(E, nx.z);
+      }
       const bool a_int = ca > N, b_int = cb > N;
       const int code0 = !a_int ? codes[size_t(ca - 1) * Pc] : 0;
       const int code1 = !b_int ? codes[size_t(cb - 1) * Pc] : 0;
