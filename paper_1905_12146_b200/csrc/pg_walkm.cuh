@@ -34,6 +34,32 @@ __device__ __forceinline__ void cpa_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
 
+// D (8 patterns x 8 NT states) = x^T M over K k-steps; with few n-tiles the
+// even/odd k-steps accumulate separately so enough independent DMMAs are in
+// flight to cover the tensor-pipe latency.
+template <int K, int NT, class F>
+__device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT][2], F bfrag) {
+  constexpr int NSPLIT = NT < 8 ? 2 : 1;
+  double acc[NSPLIT][NT][2];
+#pragma unroll
+  for (int h = 0; h < NSPLIT; ++h)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) acc[h][ni][0] = acc[h][ni][1] = 0.0;
+#pragma unroll
+  for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) dmma(acc[ki % NSPLIT][ni][0], acc[ki % NSPLIT][ni][1], x[ki], bfrag(ki, ni));
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) {
+    d[ni][0] = acc[0][ni][0];
+    d[ni][1] = acc[0][ni][1];
+    if constexpr (NSPLIT == 2) {
+      d[ni][0] += acc[NSPLIT - 1][ni][0];
+      d[ni][1] += acc[NSPLIT - 1][ni][1];
+    }
+  }
+}
+
 template <int MP>
 struct WalkMGeom {
   static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
@@ -94,47 +120,28 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       y[ki] = (t & 1) ? v1 : v0;
     }
   };
+  // DMMA chain y^T = x^T M (see dmma_chain below), then back to the A layout
+  auto chain_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return buf[(ki * 4 + t) * S + ni * 8 + q]; });
+    convert_store(d, y);
+  };
+  auto chain_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return buf[(ni * 8 + q) * S + ki * 4 + t]; });
+    convert_store(d, y);
+  };
   // e = P x with P staged column-major (TC columns): B(k, n) = P[n][k] = buf[k * S + n]
-  auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
-    double d[NT][2];
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
-#pragma unroll
-    for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-      for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], buf[(ki * 4 + t) * S + ni * 8 + q]);
-    convert_store(d, y);
-  };
+  auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { chain_P(buf, x, y); };
   // y = P^T x: B(k, n) = P[k][n] = buf[n * S + k]
-  auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
-    double d[NT][2];
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
-#pragma unroll
-    for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-      for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], buf[(ni * 8 + q) * S + ki * 4 + t]);
-    convert_store(d, y);
-  };
+  auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { chain_PT(buf, x, y); };
   // y = Q x: homogeneous Q staged row-major in smem (B(k, n) = Q[n][k] =
   // Qsm[n * S + k]); per-branch generators read from global (L1-resident)
   const bool homog = PM.homogeneous != 0;
   auto matvec_Q = [&](const double* Qm, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
-    if (homog) {
-#pragma unroll
-      for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-        for (int ni = 0; ni < NT; ++ni) dmma(d[ni][0], d[ni][1], x[ki], Qsm[(ni * 8 + q) * S + ki * 4 + t]);
-    } else {
-#pragma unroll
-      for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-        for (int ni = 0; ni < NT; ++ni)
-          dmma(d[ni][0], d[ni][1], x[ki], __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t));
-    }
+    if (homog) dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return Qsm[(ni * 8 + q) * S + ki * 4 + t]; });
+    else dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t); });
     convert_store(d, y);
   };
   auto quad_sum = [&](double v) {
@@ -211,23 +218,12 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
     auto exp_idx = [&](int node, int l) { return (size_t(node - N - 1) * L + l) * 8 + q; };
-    // bring a whole node slot (all categories) of this warp into L2 ahead of use
-    auto prefetch_slot = [&](const double* base, int node) {
-      if (node <= N) return;
-      const char* b = reinterpret_cast<const char*>(base + size_t(node - N - 1) * slotd);
-      const int lines = int(slotd * 8 / 128);
-      for (int i = lane; i < lines; i += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + size_t(i) * 128));
-    };
 
     // ------------------------------------------------ post-order pass (a)
     for (int i = 0; i < p.nsteps; ++i) {
       const int4 st = p.post[i];
       const int k = st.x;
-      if (i + 1 < p.nsteps) {  // next step's stored operands -> L2 while this step computes
-        const int4 nx = p.post[i + 1];
-        prefetch_slot(E, nx.y);
-        prefetch_slot(E, nx.z);
-      }
+
       const int code0 = st.y <= N ? codes[size_t(st.y - 1) * Pc] : 0;
       const int code1 = st.z <= N ? codes[size_t(st.z - 1) * Pc] : 0;
       Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
@@ -309,12 +305,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
     for (int i = 0; i < p.nsteps; ++i) {
       const int4 st = p.pre[i];
       const int k = st.x, ca = st.y, cb = st.z;
-      if (i + 1 < p.nsteps) {
-        const int4 nx = p.pre[i + 1];
-        if (nx.x != root) prefetch_slot(Qs, nx.x);
-        prefetch_slot(E, nx.y);
-        prefetch_slot(E, nx.z);
-      }
+
       const bool a_int = ca > N, b_int = cb > N;
       const int code0 = !a_int ? codes[size_t(ca - 1) * Pc] : 0;
       const int code1 = !b_int ? codes[size_t(cb - 1) * Pc] : 0;
