@@ -33,6 +33,8 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cpa_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // D (8 patterns x 8 NT states) = x^T M over K k-steps; with few n-tiles the
 // even/odd k-steps accumulate separately so enough independent DMMAs are in
@@ -67,22 +69,25 @@ struct WalkMGeom {
   // padded smem row stride (doubles): S % 16 == 4 makes both B-fragment access
   // patterns (row-major and column-major reads) bank-conflict free
   static constexpr int S = ((MP + 4) % 16 == 4) ? MP + 4 : MP + 12;
-  // two P(t) blocks (the children of a pre-order step) + the generator Q
-  static constexpr size_t smem_bytes() { return size_t(3 * MP * S) * sizeof(double); }
+  // small state spaces double-buffer the P(t) blocks across units
+  static constexpr bool PIPE = MP <= 32;
+  static constexpr int NPB = PIPE ? 4 : 2;
+  // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
+  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * MP * S) * sizeof(double); }
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
-  // cross-category operand prefetch: measured slower on C4 (266 vs 236 ms) because
-  // the extra registers cost a resident CTA; kept selectable
-  constexpr bool PF = false;
+  // operand prefetch into registers for the next (step, category) unit; only
+  // small state spaces have the registers for it
+  constexpr bool PF = MP <= 32;
   const WalkParams& p = PM.p;
+  constexpr bool PIPE = Gm::PIPE;
   extern __shared__ __align__(16) double smd[];
-  double* Pbuf0 = smd;
-  double* Pbuf1 = smd + MP * S;
-  double* Qsm = smd + 2 * MP * S;  // homogeneous generator, row-major, stride S
+  auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * MP * S; };
+  double* Qsm = smd + size_t(Gm::NPB) * MP * S;  // homogeneous generator, row-major, stride S
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
@@ -195,6 +200,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
     const double w = valid ? p.weights[sc] : 0.0;
     const uint8_t* codes = p.codes + sc;
     const size_t Pc = size_t(p.Pc);
+    const int n = p.nsteps, U = n * L;
+    const bool pf = PF && L > 1;  // (L == 1 would read a slot this unit is still writing)
 
     auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
       const double* src = base + size_t(node - N - 1) * slotd + size_t(l) * K * 32 + lane;
@@ -218,142 +225,190 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
     auto exp_idx = [&](int node, int l) { return (size_t(node - N - 1) * L + l) * 8 + q; };
+    auto tipcode = [&](int node) -> int { return node <= N ? int(codes[size_t(node - 1) * Pc]) : 0; };
+    auto copyv = [&](double (&dst)[K], const double (&src)[K]) {
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) dst[ki] = src[ki];
+    };
 
     // ------------------------------------------------ post-order pass (a)
-    for (int i = 0; i < p.nsteps; ++i) {
-      const int4 st = p.post[i];
-      const int k = st.x;
-
-      const int code0 = st.y <= N ? codes[size_t(st.y - 1) * Pc] : 0;
-      const int code1 = st.z <= N ? codes[size_t(st.z - 1) * Pc] : 0;
-      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
-      auto load_post = [&](int l, double (&a)[K], double (&b)[K], int& xa, int& xb) {
+    // Units (step i, category l) in lock-step.  PIPE: the next unit's P(t)
+    // block is staged into the other buffer parity while this unit computes;
+    // PF: its operands are loaded into registers as well.
+    {
+      auto load_post = [&](const int4 st, int c0, int c1, int l, double (&a)[K], double (&b)[K], int& xa, int& xb) {
         xa = xb = 0;
-        if (st.y <= N) gather(st.y, code0, l, a);
+        if (st.y <= N) gather(st.y, c0, l, a);
         else {
           load_slot(E, st.y, l, a);
           xa = Ex[exp_idx(st.y, l)];
         }
-        if (st.z <= N) gather(st.z, code1, l, b);
+        if (st.z <= N) gather(st.z, c1, l, b);
         else {
           load_slot(E, st.z, l, b);
           xb = Ex[exp_idx(st.z, l)];
         }
       };
-      // small state spaces: the next category's operands are loaded while
-      // this category computes (software pipeline over categories)
+      int4 stc = p.post[0];
+      int4 stn = n > 1 ? p.post[1] : stc;
+      int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
+      int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
+      if (PIPE && stc.x != root) stage_P(pbuf(0, 0), stc.x, 0);
+      cpa_commit();
       double an[K], bn[K];
       int xan = 0, xbn = 0;
-      if constexpr (PF) load_post(0, an, bn, xan, xbn);
-      for (int l = 0; l < L; ++l) {
+      if (pf) load_post(stc, cc0, cc1, 0, an, bn, xan, xbn);
+      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      int i = 0, l = 0;
+      for (int u = 0; u < U; ++u) {
+        const int par = PIPE ? (u & 1) : 0;
+        cpa_wait_all();
         __syncthreads();
-        if (k != root) stage_P(Pbuf0, k, l);
+        int l2 = l + 1;
+        const bool step_end = l2 == L;
+        if (step_end) l2 = 0;
+        const bool has_next = u + 1 < U;
+        const int4 st2 = step_end ? stn : stc;
+        if (PIPE) {
+          if (has_next && st2.x != root) stage_P(pbuf(0, (u + 1) & 1), st2.x, l2);
+        } else if (stc.x != root) {
+          stage_P(pbuf(0, 0), stc.x, l);
+        }
+        cpa_commit();
         double a[K], b[K];
         int xa = 0, xb = 0;
-        if constexpr (PF) {
-#pragma unroll
-          for (int ki = 0; ki < K; ++ki) {
-            a[ki] = an[ki];
-            b[ki] = bn[ki];
-          }
+        if (pf) {
+          copyv(a, an);
+          copyv(b, bn);
           xa = xan;
           xb = xbn;
-          if (l + 1 < L) load_post(l + 1, an, bn, xan, xbn);
+          if (has_next) load_post(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, an, bn, xan, xbn);
         } else {
-          load_post(l, a, b, xa, xb);
+          load_post(stc, cc0, cc1, l, a, b, xa, xb);
         }
 #pragma unroll
         for (int ki = 0; ki < K; ++ki) a[ki] *= b[ki];
-        int ex = p.disable ? 0 : quad_peak_exp(a);
+        const int ex = p.disable ? 0 : quad_peak_exp(a);
         scale_by(a, ex);
         const int Sk = xa + xb + ex;
-        if (k == root) {
+        if (stc.x == root) {
           double d = 0.0;
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) d = fma(p.pi[ki * 4 + t], a[ki], d);
           d = quad_sum(d) * p.probs[l];
-          // combine with the running mixture (rebased to the larger exponent)
           if (Sk > mix.ref) {
             mix.v[0] = mix.ref == INT_MIN ? 0.0 : mix.v[0] * pow2(mix.ref - Sk);
             mix.ref = Sk;
           }
           mix.v[0] += d * pow2(Sk - mix.ref);
+          if (step_end) {
+            const double m = mix.v[0];
+            const double ll = log(m) + double(mix.ref) * 0.6931471805599453;
+            if (owner) {
+              if (!isfinite(m)) atomicMin(&p.err[0], s);
+              else if (m <= 0.0) atomicMin(&p.err[1], s);
+              if (p.site_ll) p.site_ll[s] = ll;
+            }
+            const double v = warp_sum(owner ? w * ll : 0.0);
+            if (lane == 0) atomicAdd(Acc, v);
+          }
         } else {
-          cpa_commit_wait_all();
-          __syncthreads();
+          if (!PIPE) {
+            cpa_wait_all();
+            __syncthreads();
+          }
           double e[K];
-          matvec_P(Pbuf0, a, e);
-          store_slot(E, k, l, e);
-          if (t == 0) Ex[exp_idx(k, l)] = Sk;
+          matvec_P(pbuf(0, par), a, e);
+          store_slot(E, stc.x, l, e);
+          if (t == 0) Ex[exp_idx(stc.x, l)] = Sk;
         }
-      }
-      if (k == root) {
-        const double m = mix.v[0];
-        const double ll = log(m) + double(mix.ref) * 0.6931471805599453;
-        if (owner) {
-          if (!isfinite(m)) atomicMin(&p.err[0], s);
-          else if (m <= 0.0) atomicMin(&p.err[1], s);
-          if (p.site_ll) p.site_ll[s] = ll;
+        l = l2;
+        if (step_end) {
+          ++i;
+          mix = Mix{{0, 0, 0, 0, 0}, INT_MIN};
+          stc = stn;
+          cc0 = cn0;
+          cc1 = cn1;
+          if (i + 1 < n) {
+            stn = p.post[i + 1];
+            cn0 = tipcode(stn.y);
+            cn1 = tipcode(stn.z);
+          }
         }
-        const double v = warp_sum(owner ? w * ll : 0.0);
-        if (lane == 0) atomicAdd(Acc, v);
       }
     }
     if (!p.do_pre) continue;
 
     // ----------------------------------- pre-order pass + gradient (b)+(c)
-    for (int i = 0; i < p.nsteps; ++i) {
-      const int4 st = p.pre[i];
-      const int k = st.x, ca = st.y, cb = st.z;
-
-      const bool a_int = ca > N, b_int = cb > N;
-      const int code0 = !a_int ? codes[size_t(ca - 1) * Pc] : 0;
-      const int code1 = !b_int ? codes[size_t(cb - 1) * Pc] : 0;
-      const double* Qa = p.qtab + size_t(p.qidx[ca]) * MP * MP;
-      const double* Qb = p.qtab + size_t(p.qidx[cb]) * MP * MP;
-      // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
-      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
-      auto load_pre = [&](int l, double (&qv)[K], double (&ea)[K], double (&eb)[K], int& xq, int& xa, int& xb) {
+    {
+      auto load_pre = [&](const int4 st, int c0, int c1, int l, double (&qv)[K], double (&ea)[K], double (&eb)[K],
+                          int& xq, int& xa, int& xb) {
         xq = xa = xb = 0;
-        if (k == root) {
+        if (st.x == root) {
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
         } else {
-          load_slot(Qs, k, l, qv);
-          xq = Qx[exp_idx(k, l)];
+          load_slot(Qs, st.x, l, qv);
+          xq = Qx[exp_idx(st.x, l)];
         }
-        if (a_int) {
-          load_slot(E, ca, l, ea);
-          xa = Ex[exp_idx(ca, l)];
-        } else gather(ca, code0, l, ea);
-        if (b_int) {
-          load_slot(E, cb, l, eb);
-          xb = Ex[exp_idx(cb, l)];
-        } else gather(cb, code1, l, eb);
+        if (st.y > N) {
+          load_slot(E, st.y, l, ea);
+          xa = Ex[exp_idx(st.y, l)];
+        } else gather(st.y, c0, l, ea);
+        if (st.z > N) {
+          load_slot(E, st.z, l, eb);
+          xb = Ex[exp_idx(st.z, l)];
+        } else gather(st.z, c1, l, eb);
       };
+      auto stage_pre = [&](const int4 st, int l, int par) {
+        if (st.y > N) stage_P(pbuf(0, par), st.y, l);
+        if (st.z > N) stage_P(pbuf(1, par), st.z, l);
+      };
+      int4 stc = p.pre[0];
+      int4 stn = n > 1 ? p.pre[1] : stc;
+      int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
+      int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
+      if (PIPE) stage_pre(stc, 0, 0);
+      cpa_commit();
       double qn[K], ean[K], ebn[K];
       int xqn = 0, xan = 0, xbn = 0;
-      if constexpr (PF) load_pre(0, qn, ean, ebn, xqn, xan, xbn);
-      for (int l = 0; l < L; ++l) {
+      if (pf) load_pre(stc, cc0, cc1, 0, qn, ean, ebn, xqn, xan, xbn);
+      // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
+      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      int i = 0, l = 0;
+      for (int u = 0; u < U; ++u) {
+        const int par = PIPE ? (u & 1) : 0;
+        const int ca = stc.y, cb = stc.z;
+        const bool a_int = ca > N, b_int = cb > N;
+        cpa_wait_all();
         __syncthreads();
-        if (a_int) stage_P(Pbuf0, ca, l);
-        if (b_int) stage_P(Pbuf1, cb, l);
+        int l2 = l + 1;
+        const bool step_end = l2 == L;
+        if (step_end) l2 = 0;
+        const bool has_next = u + 1 < U;
+        const int4 st2 = step_end ? stn : stc;
+        if (PIPE) {
+          if (has_next) stage_pre(st2, l2, (u + 1) & 1);
+        } else {
+          stage_pre(stc, l, 0);
+        }
+        cpa_commit();
         double qv[K], ea[K], eb[K];
         int xq = 0, xa = 0, xb = 0;
-        if constexpr (PF) {
-#pragma unroll
-          for (int ki = 0; ki < K; ++ki) {
-            qv[ki] = qn[ki];
-            ea[ki] = ean[ki];
-            eb[ki] = ebn[ki];
-          }
+        if (pf) {
+          copyv(qv, qn);
+          copyv(ea, ean);
+          copyv(eb, ebn);
           xq = xqn;
           xa = xan;
           xb = xbn;
-          if (l + 1 < L) load_pre(l + 1, qn, ean, ebn, xqn, xan, xbn);
+          if (has_next)
+            load_pre(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, qn, ean, ebn, xqn, xan, xbn);
         } else {
-          load_pre(l, qv, ea, eb, xq, xa, xb);
+          load_pre(stc, cc0, cc1, l, qv, ea, eb, xq, xa, xb);
         }
+        const double* Qa = p.qtab + size_t(homog ? 0 : p.qidx[ca]) * MP * MP;
+        const double* Qb = p.qtab + size_t(homog ? 0 : p.qidx[cb]) * MP * MP;
         const int El = xq + xa + xb;
         double ta[K], tb[K], dd = 0.0;
 #pragma unroll
@@ -366,41 +421,39 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         double term[5];
         term[0] = wl * quad_sum(dd);
         {
-          double u[K];
-          if (a_int) matvec_Q(Qa, ea, u);
-          else gather_q(ca, code0, l, u);
+          double uu[K];
+          if (a_int) matvec_Q(Qa, ea, uu);
+          else gather_q(ca, cc0, l, uu);
           double d1 = 0.0;
 #pragma unroll
-          for (int ki = 0; ki < K; ++ki) d1 = fma(ta[ki], u[ki], d1);
+          for (int ki = 0; ki < K; ++ki) d1 = fma(ta[ki], uu[ki], d1);
           term[1] = cl * wl * quad_sum(d1);
+          term[3] = 0.0;
           if (p.hess) {
             double u2[K];
-            matvec_Q(Qa, u, u2);
+            matvec_Q(Qa, uu, u2);
             double d2 = 0.0;
 #pragma unroll
             for (int ki = 0; ki < K; ++ki) d2 = fma(ta[ki], u2[ki], d2);
             term[3] = cl * cl * wl * quad_sum(d2);
-          } else {
-            term[3] = 0.0;
           }
         }
         {
-          double u[K];
-          if (b_int) matvec_Q(Qb, eb, u);
-          else gather_q(cb, code1, l, u);
+          double uu[K];
+          if (b_int) matvec_Q(Qb, eb, uu);
+          else gather_q(cb, cc1, l, uu);
           double d1 = 0.0;
 #pragma unroll
-          for (int ki = 0; ki < K; ++ki) d1 = fma(tb[ki], u[ki], d1);
+          for (int ki = 0; ki < K; ++ki) d1 = fma(tb[ki], uu[ki], d1);
           term[2] = cl * wl * quad_sum(d1);
+          term[4] = 0.0;
           if (p.hess) {
             double u2[K];
-            matvec_Q(Qb, u, u2);
+            matvec_Q(Qb, uu, u2);
             double d2 = 0.0;
 #pragma unroll
             for (int ki = 0; ki < K; ++ki) d2 = fma(tb[ki], u2[ki], d2);
             term[4] = cl * cl * wl * quad_sum(d2);
-          } else {
-            term[4] = 0.0;
           }
         }
         if (El > mix.ref) {
@@ -410,16 +463,16 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
           }
           mix.ref = El;
         }
-        const double sc = pow2(El - mix.ref);
-        for (int r = 0; r < 5; ++r) mix.v[r] = fma(term[r], sc, mix.v[r]);
+        const double scl = pow2(El - mix.ref);
+        for (int r = 0; r < 5; ++r) mix.v[r] = fma(term[r], scl, mix.v[r]);
         // outgoing pre-partials of internal children: q_x = P_x^T top
-        if (a_int || b_int) {
-          cpa_commit_wait_all();
+        if (!PIPE && (a_int || b_int)) {
+          cpa_wait_all();
           __syncthreads();
         }
         if (a_int) {
           double qo[K];
-          matvec_PT(Pbuf0, ta, qo);
+          matvec_PT(pbuf(0, par), ta, qo);
           const int ex = quad_peak_exp(qo);
           scale_by(qo, ex);
           store_slot(Qs, ca, l, qo);
@@ -427,28 +480,41 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         }
         if (b_int) {
           double qo[K];
-          matvec_PT(Pbuf1, tb, qo);
+          matvec_PT(pbuf(1, par), tb, qo);
           const int ex = quad_peak_exp(qo);
           scale_by(qo, ex);
           store_slot(Qs, cb, l, qo);
           if (t == 0) Qx[exp_idx(cb, l)] = xq + xa + ex;
         }
-      }
-      const double inv = 1.0 / mix.v[0];
-      const double r1a = mix.v[1] * inv, r1b = mix.v[2] * inv;
-      const double ga = warp_sum(owner ? w * r1a : 0.0);
-      const double gb = warp_sum(owner ? w * r1b : 0.0);
-      if (lane == 0) {
-        atomicAdd(Acc + ca, ga);
-        atomicAdd(Acc + cb, gb);
-      }
-      if (p.hess) {
-        const double ha = warp_sum(owner ? w * (mix.v[3] * inv - r1a * r1a) : 0.0);
-        const double hb = warp_sum(owner ? w * (mix.v[4] * inv - r1b * r1b) : 0.0);
-        if (lane == 0) {
-          atomicAdd(Acc + p.B + ca, ha);
-          atomicAdd(Acc + p.B + cb, hb);
+        if (step_end) {
+          const double inv = 1.0 / mix.v[0];
+          const double r1a = mix.v[1] * inv, r1b = mix.v[2] * inv;
+          const double ga = warp_sum(owner ? w * r1a : 0.0);
+          const double gb = warp_sum(owner ? w * r1b : 0.0);
+          if (lane == 0) {
+            atomicAdd(Acc + ca, ga);
+            atomicAdd(Acc + cb, gb);
+          }
+          if (p.hess) {
+            const double ha = warp_sum(owner ? w * (mix.v[3] * inv - r1a * r1a) : 0.0);
+            const double hb = warp_sum(owner ? w * (mix.v[4] * inv - r1b * r1b) : 0.0);
+            if (lane == 0) {
+              atomicAdd(Acc + p.B + ca, ha);
+              atomicAdd(Acc + p.B + cb, hb);
+            }
+          }
+          ++i;
+          mix = Mix{{0, 0, 0, 0, 0}, INT_MIN};
+          stc = stn;
+          cc0 = cn0;
+          cc1 = cn1;
+          if (i + 1 < n) {
+            stn = p.pre[i + 1];
+            cn0 = tipcode(stn.y);
+            cn1 = tipcode(stn.z);
+          }
         }
+        l = l2;
       }
     }
   }

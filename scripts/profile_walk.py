@@ -14,7 +14,7 @@ ap.add_argument("--sites", type=int, default=100000)
 ap.add_argument("--evals", type=int, default=2)
 ap.add_argument("--hess", action="store_true")
 a = ap.parse_args()
-inst = synth.generate(a.config, sites=a.sites)
+inst = synth.generate(a.config, sites=a.sites or None)
 eng = synth.engine_for(inst)
 for i in range(a.evals):
     eng.invalidate_caches()
