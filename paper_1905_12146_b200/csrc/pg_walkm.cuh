@@ -77,12 +77,13 @@ struct WalkMGeom {
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
-  // operand prefetch into registers for the next (step, category) unit; only
-  // small state spaces have the registers for it
-  constexpr bool PF = MP <= 32;
+  // operand prefetch into registers for the next (step, category) unit:
+  // measured slower (C4 323 vs 236 ms: 168 registers + spills cost a
+  // resident CTA), kept selectable
+  constexpr bool PF = false;
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
   extern __shared__ __align__(16) double smd[];

@@ -317,3 +317,43 @@ def test_pattern_split_linearity_full_c3():
     b = synth.engine_for(inst.slice_patterns(P // 3, P)).branch_gradient()
     assert_logl(a.log_likelihood + b.log_likelihood, whole.log_likelihood, rtol=1e-12)
     assert_vec(a.branch_gradient + b.branch_gradient, whole.branch_gradient, rtol=1e-11, what="sharded gradient")
+
+
+def test_compressed_equals_raw_sites_gpu():  # test_engine.cpp:107-131 through the product
+    rng = O.Rng(31)
+    tree_o = O.Tree.random(rng, 6, 0.05, 0.8)
+    mo = O.Model.jc69()
+    cats = O.discrete_gamma(0.9, 4)
+    codes = O.simulate_states(tree_o, mo, *cats, tree_o.branch_lengths, 400, 9)
+    labels = [tree_o.labels[i] for i in range(1, 7)]
+    tree = Tree(6, tree_o.parent, tree_o.children, np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]),
+                tree_o.labels, tree_o.post_order)
+    model = SubstitutionModel.jc69()
+    rc = RateCategories(np.asarray(cats[0]), np.asarray(cats[1]))
+    comp = SitePatternAlignment.from_codes(labels, codes, 4)
+    assert comp.pattern_count() < 400
+    whole = LikelihoodEngine(tree, comp, model, rc).log_likelihood()
+    raw = SitePatternAlignment(labels, 4, codes.astype(np.int8), np.ones(400, np.int64))
+    assert LikelihoodEngine(tree, raw, model, rc).log_likelihood() == pytest.approx(whole, rel=1e-12)
+
+
+def test_linear_time_scaling_exponent():
+    """acceptance.cpp:172-217 / SPEC.md:575: analytic-gradient wall time grows
+    linearly in N (fitted log-log exponent < 1.3) at 1000 sites."""
+    import time
+
+    ns, ts = [], []
+    for tips in (64, 128, 256, 512, 1024):
+        inst = synth.generate("C1", seed=tips, sites=1000, tips=tips)
+        eng = synth.engine_for(inst)
+        eng.branch_gradient()
+        best = 1e9
+        for _ in range(5):
+            eng.invalidate_caches()
+            t0 = time.perf_counter()
+            eng.branch_gradient()
+            best = min(best, time.perf_counter() - t0)
+        ns.append(tips)
+        ts.append(best)
+    slope = np.polyfit(np.log(ns), np.log(ts), 1)[0]
+    assert slope < 1.3, (slope, ts)
