@@ -121,7 +121,7 @@ struct pg_engine {
 
   // device state
   DevBuf<uint8_t> d_codes;
-  DevBuf<double> d_qtc;
+  DevBuf<double> d_qtc, d_fpp, d_fpt, d_fq;
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err;
   DevBuf<int4> d_post, d_pre;
@@ -459,6 +459,19 @@ struct pg_engine {
     }
     for (int i = 0; i < m; ++i) pipad[size_t(i)] = pi[size_t(i)];
     d_qtab.upload(qt.data(), qt.size(), stream);
+    if (use_walkm) {
+      // generators in mma.m8n8k4 B-fragment order (y = Q x), see tc_kernel
+      const int nq = int(1 + branch_q.size()), KK = MP / 4, NT = MP / 8;
+      std::vector<double> fq(size_t(nq) * MP * MP, 0.0);
+      for (int g = 0; g < nq; ++g)
+        for (int e = 0; e < MP * MP; ++e) {
+          const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
+          const int k = 4 * ki + (lane & 3), gq = lane >> 2, n = 4 * (2 * ni + (gq & 1)) + (gq >> 1);
+          fq[size_t(g) * MP * MP + e] = qt[size_t(g) * MP * MP + size_t(n) * MP + k];
+        }
+      (void)KK;
+      d_fq.upload(fq.data(), fq.size(), stream);
+    }
     d_qidx.upload(qidx.data(), qidx.size(), stream);
     d_pi.upload(pipad.data(), pipad.size(), stream);
     if (have_eigen) {
@@ -540,7 +553,11 @@ struct pg_engine {
     d_site_ll.ensure(size_t(std::max(P, 1)));
     d_err.ensure(3);
     d_tc.ensure(size_t(B()) * L * NC * MP);
-    if (use_walkm) d_qtc.ensure(size_t(B()) * L * NC * MP);
+    if (use_walkm) {
+      d_qtc.ensure(size_t(B()) * L * NC * MP);
+      d_fpp.ensure(size_t(B()) * L * MP * MP);
+      d_fpt.ensure(size_t(B()) * L * MP * MP);
+    }
     d_post.upload(post_steps.data(), post_steps.size(), stream);
     d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
     if (!h_out) {
@@ -727,6 +744,8 @@ void pg_engine::launch_tc() {
   p.amb = d_amb.p;
   p.tc = d_tc.p;
   p.qtc = use_walkm ? d_qtc.p : nullptr;
+  p.fpp = use_walkm ? d_fpp.p : nullptr;
+  p.fpt = use_walkm ? d_fpt.p : nullptr;
   p.err = d_err.p;
   p.m = m;
   p.MP = MP;
@@ -786,6 +805,9 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     pm.p = p;
     pm.eexp = d_eexp.p;
     pm.qexp = d_qexp.p;
+    pm.fpp = d_fpp.p;
+    pm.fpt = d_fpt.p;
+    pm.fq = d_fq.p;
     pm.homogeneous = branch_q.empty() ? 1 : 0;
     void* fn = pg_walkm_kernel(MP);
     void* args[] = {&pm};

@@ -42,6 +42,8 @@ struct TcParams {
   const double* amb;    // [A][m] ambiguity partials
   double* tc;           // [B][L][NC][MP]
   double* qtc;          // optional [B][L][NC][MP]: the same columns of Q_branch * P (tip Q-e gathers)
+  double* fpp;          // optional [B][L][MP*MP]: P in DMMA B-fragment order for y = P x (walkm)
+  double* fpt;          // optional [B][L][MP*MP]: same for y = P^T x
   int* err;             // err[2] <- 1 on a negative / non-finite branch length
   int m, MP, NC, A, L, have_eigen;
 };
@@ -233,6 +235,22 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
       }
     }
     out[e] = v;
+  }
+  if (p.fpp) {
+    // B fragments of mma.m8n8k4 for the walkm kernel: element (ki, ni, lane)
+    // = M(k = 4ki + lane%4, n = sigma(ni, lane/4)), sigma(ni, g) =
+    // 4(2ni + g%2) + g/2 — the column permutation that makes D land in the
+    // A-fragment layout (no shuffles between chained mat-vecs)
+    const int KK = p.MP / 4, NT = p.MP / 8;
+    double* fp = p.fpp + (size_t(node - 1) * p.L + l) * size_t(p.MP) * p.MP;
+    double* ft = p.fpt + (size_t(node - 1) * p.L + l) * size_t(p.MP) * p.MP;
+    for (int e = threadIdx.x; e < KK * NT * 32; e += blockDim.x) {
+      const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
+      const int k = 4 * ki + (lane & 3), g = lane >> 2, n = 4 * (2 * ni + (g & 1)) + (g >> 1);
+      const bool in = k < m && n < m;
+      fp[e] = in ? R[n * m + k] : 0.0;  // y = P x: M(k, n) = P[n][k]
+      ft[e] = in ? R[k * m + n] : 0.0;  // y = P^T x: M(k, n) = P[k][n]
+    }
   }
   if (p.qtc) {
     // Q e for a tip is a column of Q P (P and Q commute, engine.hpp:260):

@@ -69,6 +69,9 @@ struct WalkMParams {
   WalkParams p;
   int* eexp;  // [TW][N-1][L][8] exponents of the stored edge messages
   int* qexp;  // [TW][N-1][L][8] exponents of the stored pre-partials
+  const double* fpp;  // [B][L][MP*MP] P in B-fragment order (y = P x)
+  const double* fpt;  // [B][L][MP*MP] (y = P^T x)
+  const double* fq;   // [nQ][MP*MP] generators in B-fragment order (y = Q x)
   int homogeneous;  // stage the shared generator in shared memory
 };
 

@@ -65,21 +65,19 @@ __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT]
 template <int MP>
 struct WalkMGeom {
   static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
-  static constexpr int NT = MP / 8;  // n-tiles (D fragments per vector per lane)
-  // padded smem row stride (doubles): S % 16 == 4 makes both B-fragment access
-  // patterns (row-major and column-major reads) bank-conflict free
-  static constexpr int S = ((MP + 4) % 16 == 4) ? MP + 4 : MP + 12;
+  static constexpr int NT = MP / 8;  // n-tiles (D fragments per vector per lane); K == 2 NT
+  static constexpr int FRAG = MP * MP;  // doubles of one matrix in B-fragment order
   // small state spaces double-buffer the P(t) blocks across units
   static constexpr bool PIPE = MP <= 32;
   static constexpr int NPB = PIPE ? 4 : 2;
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
-  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * MP * S) * sizeof(double); }
+  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG) * sizeof(double); }
 };
 
 template <int MP>
 __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
-  constexpr int K = Gm::K, NT = Gm::NT, S = Gm::S;
+  constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
   // operand prefetch into registers for the next (step, category) unit:
   // measured slower (C4 323 vs 236 ms: 168 registers + spills cost a
   // resident CTA), kept selectable
@@ -87,8 +85,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
   extern __shared__ __align__(16) double smd[];
-  auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * MP * S; };
-  double* Qsm = smd + size_t(Gm::NPB) * MP * S;  // homogeneous generator, row-major, stride S
+  auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
+  double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
@@ -103,52 +101,39 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
   for (int i = lane; i < p.accw; i += 32) Acc[i] = 0.0;
   __syncwarp();
 
-  // stage the first MP columns (post: P) of one (node, category) TC block,
-  // rows padded to stride S; element (row r, col c) of P at buf[c * S + r]
-  auto stage_P = [&](double* buf, int node, int l) {
-    const double* src = p.tc + (size_t(node - 1) * L + l) * size_t(NC) * MP;
-    constexpr int CH = MP / 2;  // 16 B chunks per column
-    for (int i = tid; i < MP * CH; i += 128) {
-      const int c = i / CH, h = i % CH;
-      cpa16(buf + c * S + 2 * h, src + c * MP + 2 * h);
-    }
+  // stage one (node, category) matrix in B-fragment order (contiguous copy)
+  auto stage_P = [&](double* buf, const double* tab, int node, int l) {
+    const double* src = tab + (size_t(node - 1) * L + l) * size_t(FRAG);
+    for (int i = tid; i < FRAG / 2; i += 128) cpa16(buf + 2 * i, src + 2 * i);
   };
-  // D fragments (lane (q,t) holds states 8ni + 2t, 8ni + 2t + 1) -> A layout
-  // (lane (q,t) holds states 4ki + t): state 8ni + 4h + t lives in lane
-  // 4q + 2h + t/2, element t%2 — two shuffles per k-step, no shared memory.
-  auto convert_store = [&](double (&d)[NT][2], double (&y)[K]) {
+  // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
+  // frag[(ki * NT + ni) * 32 + lane]; with the permuted columns baked into the
+  // fragment tables, D tile ni holds y's A-layout entries 2ni and 2ni+1.
+  auto matvec = [&](const double* frag, const double (&x)[K], double (&y)[K]) {
+    double d[NT][2];
+    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return frag[(ki * NT + ni) * 32 + lane]; });
 #pragma unroll
-    for (int ki = 0; ki < K; ++ki) {
-      const int ni = ki >> 1, h = ki & 1;
-      const int src = (q << 2) + 2 * h + (t >> 1);
-      const double v0 = __shfl_sync(kFull, d[ni][0], src);
-      const double v1 = __shfl_sync(kFull, d[ni][1], src);
-      y[ki] = (t & 1) ? v1 : v0;
+    for (int ni = 0; ni < NT; ++ni) {
+      y[2 * ni] = d[ni][0];
+      y[2 * ni + 1] = d[ni][1];
     }
   };
-  // DMMA chain y^T = x^T M (see dmma_chain below), then back to the A layout
-  auto chain_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
+  auto matvec_g = [&](const double* frag, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
-    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return buf[(ki * 4 + t) * S + ni * 8 + q]; });
-    convert_store(d, y);
+    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return __ldg(frag + (ki * NT + ni) * 32 + lane); });
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      y[2 * ni] = d[ni][0];
+      y[2 * ni + 1] = d[ni][1];
+    }
   };
-  auto chain_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) {
-    double d[NT][2];
-    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return buf[(ni * 8 + q) * S + ki * 4 + t]; });
-    convert_store(d, y);
-  };
-  // e = P x with P staged column-major (TC columns): B(k, n) = P[n][k] = buf[k * S + n]
-  auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { chain_P(buf, x, y); };
-  // y = P^T x: B(k, n) = P[k][n] = buf[n * S + k]
-  auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { chain_PT(buf, x, y); };
-  // y = Q x: homogeneous Q staged row-major in smem (B(k, n) = Q[n][k] =
-  // Qsm[n * S + k]); per-branch generators read from global (L1-resident)
+  auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
+  auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
+  // homogeneous Q staged in smem; per-branch generators read in fragment order from global
   const bool homog = PM.homogeneous != 0;
-  auto matvec_Q = [&](const double* Qm, const double (&x)[K], double (&y)[K]) {
-    double d[NT][2];
-    if (homog) dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return Qsm[(ni * 8 + q) * S + ki * 4 + t]; });
-    else dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return __ldg(Qm + (ni * 8 + q) * MP + ki * 4 + t); });
-    convert_store(d, y);
+  auto matvec_Q = [&](const double* Qf, const double (&x)[K], double (&y)[K]) {
+    if (homog) matvec(Qsm, x, y);
+    else matvec_g(Qf, x, y);
   };
   auto quad_sum = [&](double v) {
     v += __shfl_xor_sync(kFull, v, 1);
@@ -189,7 +174,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
   };
 
   if (homog) {
-    for (int i = tid; i < MP * MP; i += 128) Qsm[(i / MP) * S + (i % MP)] = p.qtab[i];
+    for (int i = tid; i < FRAG; i += 128) Qsm[i] = PM.fq[i];
     __syncthreads();
   }
 
@@ -254,7 +239,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       int4 stn = n > 1 ? p.post[1] : stc;
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
-      if (PIPE && stc.x != root) stage_P(pbuf(0, 0), stc.x, 0);
+      if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0);
       cpa_commit();
       double an[K], bn[K];
       int xan = 0, xbn = 0;
@@ -271,9 +256,9 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         const bool has_next = u + 1 < U;
         const int4 st2 = step_end ? stn : stc;
         if (PIPE) {
-          if (has_next && st2.x != root) stage_P(pbuf(0, (u + 1) & 1), st2.x, l2);
+          if (has_next && st2.x != root) stage_P(pbuf(0, (u + 1) & 1), PM.fpp, st2.x, l2);
         } else if (stc.x != root) {
-          stage_P(pbuf(0, 0), stc.x, l);
+          stage_P(pbuf(0, 0), PM.fpp, stc.x, l);
         }
         cpa_commit();
         double a[K], b[K];
@@ -362,8 +347,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         } else gather(st.z, c1, l, eb);
       };
       auto stage_pre = [&](const int4 st, int l, int par) {
-        if (st.y > N) stage_P(pbuf(0, par), st.y, l);
-        if (st.z > N) stage_P(pbuf(1, par), st.z, l);
+        if (st.y > N) stage_P(pbuf(0, par), PM.fpt, st.y, l);
+        if (st.z > N) stage_P(pbuf(1, par), PM.fpt, st.z, l);
       };
       int4 stc = p.pre[0];
       int4 stn = n > 1 ? p.pre[1] : stc;
@@ -408,8 +393,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         } else {
           load_pre(stc, cc0, cc1, l, qv, ea, eb, xq, xa, xb);
         }
-        const double* Qa = p.qtab + size_t(homog ? 0 : p.qidx[ca]) * MP * MP;
-        const double* Qb = p.qtab + size_t(homog ? 0 : p.qidx[cb]) * MP * MP;
+        const double* Qa = PM.fq + size_t(homog ? 0 : p.qidx[ca]) * FRAG;
+        const double* Qb = PM.fq + size_t(homog ? 0 : p.qidx[cb]) * FRAG;
         const int El = xq + xa + xb;
         double ta[K], tb[K], dd = 0.0;
 #pragma unroll
