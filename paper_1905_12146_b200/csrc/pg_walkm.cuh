@@ -33,6 +33,14 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cpa_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -67,15 +75,18 @@ struct WalkMGeom {
   static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
   static constexpr int NT = MP / 8;  // n-tiles (D fragments per vector per lane); K == 2 NT
   static constexpr int FRAG = MP * MP;  // doubles of one matrix in B-fragment order
-  // small state spaces double-buffer the P(t) blocks across units
+  // small state spaces double-buffer the P(t) blocks across units and stage
+  // the next unit's operands in shared memory (SOP)
   static constexpr bool PIPE = MP <= 32;
   static constexpr int NPB = PIPE ? 4 : 2;
-  // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
-  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG) * sizeof(double); }
+  // per warp: 2 stages x 3 operands x K x 32 doubles + 2 x 3 x 32 exponents
+  static constexpr int SOPD = PIPE ? (6 * K * 32 + 6 * 32 / 2) : 0;
+  // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q + SOP
+  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + 4 * SOPD) * sizeof(double); }
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
   // operand prefetch into registers for the next (step, category) unit:
@@ -87,6 +98,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
   extern __shared__ __align__(16) double smd[];
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
+  double* sop_base = smd + size_t(Gm::NPB + 1) * FRAG + size_t(threadIdx.x >> 5) * Gm::SOPD;
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
@@ -188,16 +200,55 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
     const size_t Pc = size_t(p.Pc);
     const int n = p.nsteps, U = n * L;
     const bool pf = PF && L > 1;  // (L == 1 would read a slot this unit is still writing)
+    const bool sop = PIPE && L > 1;
 
+    // slot layout: [category][k-step pair][lane] double2 (512 B per warp access)
+    auto slot_ptr = [&](const double* base, int node, int l) {
+      return reinterpret_cast<const double2*>(base + size_t(node - N - 1) * slotd + size_t(l) * K * 32) + lane;
+    };
     auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
-      const double* src = base + size_t(node - N - 1) * slotd + size_t(l) * K * 32 + lane;
+      const double2* src = slot_ptr(base, node, l);
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) v[ki] = __ldcg(src + ki * 32);
+      for (int kp = 0; kp < K / 2; ++kp) {
+        const double2 d = __ldcg(src + kp * 32);
+        v[2 * kp] = d.x;
+        v[2 * kp + 1] = d.y;
+      }
     };
     auto store_slot = [&](double* base, int node, int l, const double (&v)[K]) {
-      double* dst = base + size_t(node - N - 1) * slotd + size_t(l) * K * 32 + lane;
+      double2* dst = const_cast<double2*>(slot_ptr(base, node, l));
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) __stcg(dst + ki * 32, v[ki]);
+      for (int kp = 0; kp < K / 2; ++kp) __stcg(dst + kp * 32, make_double2(v[2 * kp], v[2 * kp + 1]));
+    };
+    // ---- staged operands (SOP): the next unit's operands are copied into a
+    // per-warp shared stage with cp.async while this unit computes
+    auto opbuf = [&](int stage, int which) -> double* { return sop_base + (stage * 3 + which) * (K * 32); };
+    auto xpbuf = [&](int stage, int which) -> int* {
+      return reinterpret_cast<int*>(sop_base + 6 * (K * 32)) + (stage * 3 + which) * 32;
+    };
+    auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l, const int* xsrc) {
+      const double2* src = slot_ptr(base, node, l);
+      double2* dst = reinterpret_cast<double2*>(opbuf(stage, which)) + lane;
+#pragma unroll
+      for (int kp = 0; kp < K / 2; ++kp) cpa16(dst + kp * 32, src + kp * 32);
+      cpa4(xpbuf(stage, which) + lane, xsrc);
+    };
+    auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
+      const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+      double* dst = opbuf(stage, which);
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) cpa8(dst + ((ki >> 1) * 32 + lane) * 2 + (ki & 1), col + ki * 4);
+      xpbuf(stage, which)[lane] = 0;
+    };
+    auto read_op = [&](int stage, int which, double (&v)[K], int& x) {
+      const double2* src = reinterpret_cast<const double2*>(opbuf(stage, which)) + lane;
+#pragma unroll
+      for (int kp = 0; kp < K / 2; ++kp) {
+        const double2 d = src[kp * 32];
+        v[2 * kp] = d.x;
+        v[2 * kp + 1] = d.y;
+      }
+      x = xpbuf(stage, which)[lane];
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
       const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
@@ -239,7 +290,14 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       int4 stn = n > 1 ? p.post[1] : stc;
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
+      auto stage_post_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
+        if (st.y <= N) stage_gather_op(stage, 0, st.y, c0, l);
+        else stage_slot_op(stage, 0, E, st.y, l, Ex + exp_idx(st.y, l));
+        if (st.z <= N) stage_gather_op(stage, 1, st.z, c1, l);
+        else stage_slot_op(stage, 1, E, st.z, l, Ex + exp_idx(st.z, l));
+      };
       if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0);
+      if (sop) stage_post_ops(stc, cc0, cc1, 0, 0);
       cpa_commit();
       double an[K], bn[K];
       int xan = 0, xbn = 0;
@@ -257,13 +315,17 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         const int4 st2 = step_end ? stn : stc;
         if (PIPE) {
           if (has_next && st2.x != root) stage_P(pbuf(0, (u + 1) & 1), PM.fpp, st2.x, l2);
+          if (sop && has_next) stage_post_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
         } else if (stc.x != root) {
           stage_P(pbuf(0, 0), PM.fpp, stc.x, l);
         }
         cpa_commit();
         double a[K], b[K];
         int xa = 0, xb = 0;
-        if (pf) {
+        if (sop) {
+          read_op(u & 1, 0, a, xa);
+          read_op(u & 1, 1, b, xb);
+        } else if (pf) {
           copyv(a, an);
           copyv(b, bn);
           xa = xan;
@@ -354,7 +416,15 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
       int4 stn = n > 1 ? p.pre[1] : stc;
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
+      auto stage_pre_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
+        if (st.x != root) stage_slot_op(stage, 2, Qs, st.x, l, Qx + exp_idx(st.x, l));
+        if (st.y > N) stage_slot_op(stage, 0, E, st.y, l, Ex + exp_idx(st.y, l));
+        else stage_gather_op(stage, 0, st.y, c0, l);
+        if (st.z > N) stage_slot_op(stage, 1, E, st.z, l, Ex + exp_idx(st.z, l));
+        else stage_gather_op(stage, 1, st.z, c1, l);
+      };
       if (PIPE) stage_pre(stc, 0, 0);
+      if (sop) stage_pre_ops(stc, cc0, cc1, 0, 0);
       cpa_commit();
       double qn[K], ean[K], ebn[K];
       int xqn = 0, xan = 0, xbn = 0;
@@ -375,13 +445,23 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 4 : 2)) walkm_kernel(const __
         const int4 st2 = step_end ? stn : stc;
         if (PIPE) {
           if (has_next) stage_pre(st2, l2, (u + 1) & 1);
+          if (sop && has_next) stage_pre_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
         } else {
           stage_pre(stc, l, 0);
         }
         cpa_commit();
         double qv[K], ea[K], eb[K];
         int xq = 0, xa = 0, xb = 0;
-        if (pf) {
+        if (sop) {
+          if (stc.x == root) {
+#pragma unroll
+            for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
+          } else {
+            read_op(u & 1, 2, qv, xq);
+          }
+          read_op(u & 1, 0, ea, xa);
+          read_op(u & 1, 1, eb, xb);
+        } else if (pf) {
           copyv(qv, qn);
           copyv(ea, ean);
           copyv(eb, ebn);
