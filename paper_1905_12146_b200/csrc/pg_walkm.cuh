@@ -70,6 +70,24 @@ __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT]
   }
 }
 
+// Two independent chains interleaved (the two children of a pre-order step):
+// twice the DMMAs in flight; a shared B operand is loaded once.
+template <int K, int NT, class FA, class FB>
+__device__ __forceinline__ void dmma_chain2(const double (&xa)[K], double (&da)[NT][2], FA fa, const double (&xb)[K],
+                                            double (&db)[NT][2], FB fb, bool shared_b) {
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) da[ni][0] = da[ni][1] = db[ni][0] = db[ni][1] = 0.0;
+#pragma unroll
+  for (int ki = 0; ki < K; ++ki)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const double ba = fa(ki, ni);
+      const double bb = shared_b ? ba : fb(ki, ni);
+      dmma(da[ni][0], da[ni][1], xa[ki], ba);
+      dmma(db[ni][0], db[ni][1], xb[ki], bb);
+    }
+}
+
 template <int MP>
 struct WalkMGeom {
   static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
@@ -138,6 +156,28 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
       y[2 * ni] = d[ni][0];
       y[2 * ni + 1] = d[ni][1];
     }
+  };
+  auto unpack = [&](double (&d)[NT][2], double (&y)[K]) {
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      y[2 * ni] = d[ni][0];
+      y[2 * ni + 1] = d[ni][1];
+    }
+  };
+  // two mat-vecs with smem (or, if g, global) fragments, interleaved
+  auto matvec2 = [&](const double* fa, const double (&xa)[K], double (&ya)[K], const double* fb,
+                     const double (&xb)[K], double (&yb)[K], bool g) {
+    double da[NT][2], db[NT][2];
+    if (g)
+      dmma_chain2<K, NT>(
+          xa, da, [&](int ki, int ni) { return __ldg(fa + (ki * NT + ni) * 32 + lane); }, xb, db,
+          [&](int ki, int ni) { return __ldg(fb + (ki * NT + ni) * 32 + lane); }, fa == fb);
+    else
+      dmma_chain2<K, NT>(
+          xa, da, [&](int ki, int ni) { return fa[(ki * NT + ni) * 32 + lane]; }, xb, db,
+          [&](int ki, int ni) { return fb[(ki * NT + ni) * 32 + lane]; }, fa == fb);
+    unpack(da, ya);
+    unpack(db, yb);
   };
   auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
   auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
@@ -486,40 +526,36 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
         const double wl = p.probs[l], cl = p.rates[l];
         double term[5];
         term[0] = wl * quad_sum(dd);
+        term[3] = term[4] = 0.0;
         {
-          double uu[K];
-          if (a_int) matvec_Q(Qa, ea, uu);
-          else gather_q(ca, cc0, l, uu);
-          double d1 = 0.0;
-#pragma unroll
-          for (int ki = 0; ki < K; ++ki) d1 = fma(ta[ki], uu[ki], d1);
-          term[1] = cl * wl * quad_sum(d1);
-          term[3] = 0.0;
-          if (p.hess) {
-            double u2[K];
-            matvec_Q(Qa, uu, u2);
-            double d2 = 0.0;
-#pragma unroll
-            for (int ki = 0; ki < K; ++ki) d2 = fma(ta[ki], u2[ki], d2);
-            term[3] = cl * cl * wl * quad_sum(d2);
+          double ua[K], ub[K];
+          if (a_int && b_int) {
+            matvec2(homog ? Qsm : Qa, ea, ua, homog ? Qsm : Qb, eb, ub, !homog);
+          } else {
+            if (a_int) matvec_Q(Qa, ea, ua);
+            else gather_q(ca, cc0, l, ua);
+            if (b_int) matvec_Q(Qb, eb, ub);
+            else gather_q(cb, cc1, l, ub);
           }
-        }
-        {
-          double uu[K];
-          if (b_int) matvec_Q(Qb, eb, uu);
-          else gather_q(cb, cc1, l, uu);
-          double d1 = 0.0;
+          double d1a = 0.0, d1b = 0.0;
 #pragma unroll
-          for (int ki = 0; ki < K; ++ki) d1 = fma(tb[ki], uu[ki], d1);
-          term[2] = cl * wl * quad_sum(d1);
-          term[4] = 0.0;
+          for (int ki = 0; ki < K; ++ki) {
+            d1a = fma(ta[ki], ua[ki], d1a);
+            d1b = fma(tb[ki], ub[ki], d1b);
+          }
+          term[1] = cl * wl * quad_sum(d1a);
+          term[2] = cl * wl * quad_sum(d1b);
           if (p.hess) {
-            double u2[K];
-            matvec_Q(Qb, uu, u2);
-            double d2 = 0.0;
+            double u2a[K], u2b[K];
+            matvec2(homog ? Qsm : Qa, ua, u2a, homog ? Qsm : Qb, ub, u2b, !homog);
+            double d2a = 0.0, d2b = 0.0;
 #pragma unroll
-            for (int ki = 0; ki < K; ++ki) d2 = fma(tb[ki], u2[ki], d2);
-            term[4] = cl * cl * wl * quad_sum(d2);
+            for (int ki = 0; ki < K; ++ki) {
+              d2a = fma(ta[ki], u2a[ki], d2a);
+              d2b = fma(tb[ki], u2b[ki], d2b);
+            }
+            term[3] = cl * cl * wl * quad_sum(d2a);
+            term[4] = cl * cl * wl * quad_sum(d2b);
           }
         }
         if (El > mix.ref) {
@@ -536,21 +572,25 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
           cpa_wait_all();
           __syncthreads();
         }
-        if (a_int) {
+        auto emit_q = [&](int x, double (&qo)[K], int xbase) {
+          const int ex = quad_peak_exp(qo);
+          scale_by(qo, ex);
+          store_slot(Qs, x, l, qo);
+          if (t == 0) Qx[exp_idx(x, l)] = xbase + ex;
+        };
+        if (a_int && b_int) {
+          double qa_[K], qb_[K];
+          matvec2(pbuf(0, par), ta, qa_, pbuf(1, par), tb, qb_, false);
+          emit_q(ca, qa_, xq + xb);
+          emit_q(cb, qb_, xq + xa);
+        } else if (a_int) {
           double qo[K];
           matvec_PT(pbuf(0, par), ta, qo);
-          const int ex = quad_peak_exp(qo);
-          scale_by(qo, ex);
-          store_slot(Qs, ca, l, qo);
-          if (t == 0) Qx[exp_idx(ca, l)] = xq + xb + ex;
-        }
-        if (b_int) {
+          emit_q(ca, qo, xq + xb);
+        } else if (b_int) {
           double qo[K];
           matvec_PT(pbuf(1, par), tb, qo);
-          const int ex = quad_peak_exp(qo);
-          scale_by(qo, ex);
-          store_slot(Qs, cb, l, qo);
-          if (t == 0) Qx[exp_idx(cb, l)] = xq + xa + ex;
+          emit_q(cb, qo, xq + xa);
         }
         if (step_end) {
           const double inv = 1.0 / mix.v[0];
