@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
   // measured slower (C4 323 vs 236 ms: 168 registers + spills cost a
   // resident CTA), kept selectable
   constexpr bool PF = false;
+  // interleave the two children's mat-vecs (small state spaces: short chains)
+  constexpr bool DUAL = MP <= 32;
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
   extern __shared__ __align__(16) double smd[];
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
         term[3] = term[4] = 0.0;
         {
           double ua[K], ub[K];
-          if (a_int && b_int) {
+          if (DUAL && a_int && b_int) {
             matvec2(homog ? Qsm : Qa, ea, ua, homog ? Qsm : Qb, eb, ub, !homog);
           } else {
             if (a_int) matvec_Q(Qa, ea, ua);
@@ -547,7 +549,12 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
           term[2] = cl * wl * quad_sum(d1b);
           if (p.hess) {
             double u2a[K], u2b[K];
-            matvec2(homog ? Qsm : Qa, ua, u2a, homog ? Qsm : Qb, ub, u2b, !homog);
+            if (DUAL) {
+              matvec2(homog ? Qsm : Qa, ua, u2a, homog ? Qsm : Qb, ub, u2b, !homog);
+            } else {
+              matvec_Q(Qa, ua, u2a);
+              matvec_Q(Qb, ub, u2b);
+            }
             double d2a = 0.0, d2b = 0.0;
 #pragma unroll
             for (int ki = 0; ki < K; ++ki) {
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
           store_slot(Qs, x, l, qo);
           if (t == 0) Qx[exp_idx(x, l)] = xbase + ex;
         };
-        if (a_int && b_int) {
+        if (DUAL && a_int && b_int) {
           double qa_[K], qb_[K];
           matvec2(pbuf(0, par), ta, qa_, pbuf(1, par), tb, qb_, false);
           emit_q(ca, qa_, xq + xb);
