@@ -28,6 +28,7 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv) {
 int pg_walk4_nc(int nc);
 void* pg_walkm_kernel(int mp);
 size_t pg_walkm_smem(int mp);
+int pg_walkm_wpc(int mp);
 
 void* pg_walk_kernel_small(int MP, int LC);
 void* pg_walk_kernel_mid(int MP, int LC);
@@ -114,6 +115,7 @@ struct pg_engine {
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
   bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
+  int walkm_wpc = 4;       // warps per CTA in walkm
   DevBuf<int> d_eexp, d_qexp;
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
   size_t walk_smem = 0;
@@ -461,13 +463,13 @@ struct pg_engine {
     d_qtab.upload(qt.data(), qt.size(), stream);
     if (use_walkm) {
       // generators in mma.m8n8k4 B-fragment order (y = Q x), see tc_kernel
-      const int nq = int(1 + branch_q.size()), KK = MP / 4, NT = MP / 8;
-      std::vector<double> fq(size_t(nq) * MP * MP, 0.0);
+      const int nq = int(1 + branch_q.size()), KK = MP / 4, NT = (KK + 1) / 2, frag = KK * NT * 32;
+      std::vector<double> fq(size_t(nq) * frag, 0.0);
       for (int g = 0; g < nq; ++g)
-        for (int e = 0; e < MP * MP; ++e) {
+        for (int e = 0; e < frag; ++e) {
           const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
           const int k = 4 * ki + (lane & 3), gq = lane >> 2, n = 4 * (2 * ni + (gq & 1)) + (gq >> 1);
-          fq[size_t(g) * MP * MP + e] = qt[size_t(g) * MP * MP + size_t(n) * MP + k];
+          if (n < MP) fq[size_t(g) * frag + e] = qt[size_t(g) * MP * MP + size_t(n) * MP + k];
         }
       (void)KK;
       d_fq.upload(fq.data(), fq.size(), stream);
@@ -490,7 +492,7 @@ struct pg_engine {
 
   void prepare_geometry() {
     use_walkm = m > 8 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
-    if (use_walkm) MP = m <= 24 ? 24 : m <= 32 ? 32 : 64;
+    if (use_walkm) MP = m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
     else MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
     int nc4 = 0;
@@ -523,10 +525,11 @@ struct pg_engine {
       use_walk4 = false;
       LC = 1;
       G = 4;  // a quad of lanes per pattern (DMMA fragment layout)
-      ntiles = (P + 31) / 32;  // CTA tiles of 32 patterns
+      walkm_wpc = pg_walkm_wpc(MP);
+      ntiles = (P + 8 * walkm_wpc - 1) / (8 * walkm_wpc);  // CTA tiles of 8 patterns per warp
       walk_smem = pg_walkm_smem(MP);
     }
-    const int maxw = walk_max_blocks_per_sm() * num_sms * pgk::kWarpsPerBlock;
+    const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : pgk::kWarpsPerBlock);
     const size_t vec = use_walkm ? size_t(L) * 8 * MP : size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
     size_t free_b = 0, total_b = 0;
@@ -535,8 +538,8 @@ struct pg_engine {
     int cap = int(std::max<size_t>(1, budget / per_warp));
     if (use_walkm) {
       // CTA tiles: 4 warps per tile
-      int ctas = std::max(1, std::min({maxw / 4, std::max(ntiles, 1), std::max(cap / 4, 1)}));
-      TW = ctas * 4;
+      int ctas = std::max(1, std::min({maxw / walkm_wpc, std::max(ntiles, 1), std::max(cap / walkm_wpc, 1)}));
+      TW = ctas * walkm_wpc;
     } else {
       TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
       TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
@@ -555,8 +558,9 @@ struct pg_engine {
     d_tc.ensure(size_t(B()) * L * NC * MP);
     if (use_walkm) {
       d_qtc.ensure(size_t(B()) * L * NC * MP);
-      d_fpp.ensure(size_t(B()) * L * MP * MP);
-      d_fpt.ensure(size_t(B()) * L * MP * MP);
+      const size_t frag = size_t(MP / 4) * ((MP / 4 + 1) / 2) * 32;  // WalkMGeom<MP>::FRAG
+      d_fpp.ensure(size_t(B()) * L * frag);
+      d_fpt.ensure(size_t(B()) * L * frag);
     }
     d_post.upload(post_steps.data(), post_steps.size(), stream);
     d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
@@ -714,7 +718,7 @@ int pg_engine::walk_max_blocks_per_sm() {
   if (use_walkm) {
     const void* fn = pg_walkm_kernel(MP);
     PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, walk_smem));
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 * walkm_wpc, walk_smem));
     return std::max(nb, 1);
   }
   if (use_walk4) {
@@ -811,7 +815,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     pm.homogeneous = branch_q.empty() ? 1 : 0;
     void* fn = pg_walkm_kernel(MP);
     void* args[] = {&pm};
-    PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / 4)), dim3(128), args, walk_smem, stream));
+    PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / walkm_wpc)), dim3(32 * walkm_wpc), args, walk_smem, stream));
     return;
   }
   if (use_walk4) {

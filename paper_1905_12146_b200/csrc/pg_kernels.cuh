@@ -241,9 +241,9 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
     // = M(k = 4ki + lane%4, n = sigma(ni, lane/4)), sigma(ni, g) =
     // 4(2ni + g%2) + g/2 — the column permutation that makes D land in the
     // A-fragment layout (no shuffles between chained mat-vecs)
-    const int KK = p.MP / 4, NT = p.MP / 8;
-    double* fp = p.fpp + (size_t(node - 1) * p.L + l) * size_t(p.MP) * p.MP;
-    double* ft = p.fpt + (size_t(node - 1) * p.L + l) * size_t(p.MP) * p.MP;
+    const int KK = p.MP / 4, NT = (KK + 1) / 2, frag = KK * NT * 32;
+    double* fp = p.fpp + (size_t(node - 1) * p.L + l) * size_t(frag);
+    double* ft = p.fpt + (size_t(node - 1) * p.L + l) * size_t(frag);
     for (int e = threadIdx.x; e < KK * NT * 32; e += blockDim.x) {
       const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
       const int k = 4 * ki + (lane & 3), g = lane >> 2, n = 4 * (2 * ni + (g & 1)) + (g >> 1);

@@ -88,23 +88,39 @@ __device__ __forceinline__ void dmma_chain2(const double (&xa)[K], double (&da)[
     }
 }
 
+// Resident CTAs per SM for MP <= 32: 4 caps registers at 128 (C4: 204 ms vs
+// 211 ms at 3 CTAs / 168 registers).
+#ifndef PG_WALKM_MINB_SMALL
+#define PG_WALKM_MINB_SMALL 4
+#endif
+#ifndef PG_WALKM_WPC_SMALL
+#define PG_WALKM_WPC_SMALL 4
+#endif
+
 template <int MP>
 struct WalkMGeom {
-  static constexpr int K = MP / 4;   // k-steps (A fragments per vector per lane)
-  static constexpr int NT = MP / 8;  // n-tiles (D fragments per vector per lane); K == 2 NT
-  static constexpr int FRAG = MP * MP;  // doubles of one matrix in B-fragment order
+  static_assert(MP % 4 == 0, "MP: whole k-steps");
+  static constexpr int K = MP / 4;         // k-steps (A fragments per vector per lane)
+  static constexpr int NT = (K + 1) / 2;   // n-tiles (D fragments per vector per lane); odd K drops
+                                           // the last D entry (padded output columns)
+  static constexpr int FRAG = K * NT * 32;  // doubles of one matrix in B-fragment order
   // small state spaces double-buffer the P(t) blocks across units and stage
   // the next unit's operands in shared memory (SOP)
   static constexpr bool PIPE = MP <= 32;
   static constexpr int NPB = PIPE ? 4 : 2;
+  static constexpr bool SOP = MP <= 32;
+  // warps per CTA (lock-step group sharing each staged matrix).  Measured on
+  // C5: 8 warps with double-buffered 32 KB codon blocks (one CTA per SM) is
+  // slower than two 4-warp CTAs (432 vs 423 ms).
+  static constexpr int WPC = MP <= 32 ? PG_WALKM_WPC_SMALL : 4;
   // per warp: 2 stages x 3 operands x K x 32 doubles + 2 x 3 x 32 exponents
-  static constexpr int SOPD = PIPE ? (6 * K * 32 + 6 * 32 / 2) : 0;
+  static constexpr int SOPD = SOP ? (6 * K * 32 + 6 * 32 / 2) : 0;
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q + SOP
-  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + 4 * SOPD) * sizeof(double); }
+  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD) * sizeof(double); }
 };
 
 template <int MP>
-__global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
+__global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_MINB_SMALL : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
   // operand prefetch into registers for the next (step, category) unit:
@@ -122,8 +138,9 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
-  const int warp = blockIdx.x * 4 + wib;
-  const int ntile_cta = (p.P + 31) / 32;
+  constexpr int WPC = Gm::WPC, CT = 32 * WPC;  // warps / threads per CTA
+  const int warp = blockIdx.x * WPC + wib;
+  const int ntile_cta = (p.P + 8 * WPC - 1) / (8 * WPC);
   const size_t slotd = size_t(L) * K * 32;  // doubles per node slot per warp
   double* E = p.escr + size_t(warp) * size_t(N - 1) * slotd;
   double* Qs = p.qscr + size_t(warp) * size_t(N - 1) * slotd;
@@ -136,7 +153,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
   // stage one (node, category) matrix in B-fragment order (contiguous copy)
   auto stage_P = [&](double* buf, const double* tab, int node, int l) {
     const double* src = tab + (size_t(node - 1) * L + l) * size_t(FRAG);
-    for (int i = tid; i < FRAG / 2; i += 128) cpa16(buf + 2 * i, src + 2 * i);
+    for (int i = tid; i < FRAG / 2; i += CT) cpa16(buf + 2 * i, src + 2 * i);
   };
   // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
   // frag[(ki * NT + ni) * 32 + lane]; with the permuted columns baked into the
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       y[2 * ni] = d[ni][0];
-      y[2 * ni + 1] = d[ni][1];
+      if (2 * ni + 1 < K) y[2 * ni + 1] = d[ni][1];
     }
   };
   auto matvec_g = [&](const double* frag, const double (&x)[K], double (&y)[K]) {
@@ -156,14 +173,14 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       y[2 * ni] = d[ni][0];
-      y[2 * ni + 1] = d[ni][1];
+      if (2 * ni + 1 < K) y[2 * ni + 1] = d[ni][1];
     }
   };
   auto unpack = [&](double (&d)[NT][2], double (&y)[K]) {
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       y[2 * ni] = d[ni][0];
-      y[2 * ni + 1] = d[ni][1];
+      if (2 * ni + 1 < K) y[2 * ni + 1] = d[ni][1];
     }
   };
   // two mat-vecs with smem (or, if g, global) fragments, interleaved
@@ -228,12 +245,12 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
   };
 
   if (homog) {
-    for (int i = tid; i < FRAG; i += 128) Qsm[i] = PM.fq[i];
+    for (int i = tid; i < FRAG; i += CT) Qsm[i] = PM.fq[i];
     __syncthreads();
   }
 
   for (int tile = blockIdx.x; tile < ntile_cta; tile += gridDim.x) {
-    const int s = tile * 32 + wib * 8 + q;
+    const int s = tile * (8 * WPC) + wib * 8 + q;
     const bool valid = s < p.P;
     const bool owner = valid && t == 0;
     const int sc = valid ? s : p.P - 1;
@@ -242,9 +259,10 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
     const size_t Pc = size_t(p.Pc);
     const int n = p.nsteps, U = n * L;
     const bool pf = PF && L > 1;  // (L == 1 would read a slot this unit is still writing)
-    const bool sop = PIPE && L > 1;
+    const bool sop = Gm::SOP && L > 1;
 
-    // slot layout: [category][k-step pair][lane] double2 (512 B per warp access)
+    // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
+    // an odd last k-step as [lane] double
     auto slot_ptr = [&](const double* base, int node, int l) {
       return reinterpret_cast<const double2*>(base + size_t(node - N - 1) * slotd + size_t(l) * K * 32) + lane;
     };
@@ -256,11 +274,13 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
         v[2 * kp] = d.x;
         v[2 * kp + 1] = d.y;
       }
+      if constexpr (K & 1) v[K - 1] = __ldcg(reinterpret_cast<const double*>(src - lane + (K / 2) * 32) + lane);
     };
     auto store_slot = [&](double* base, int node, int l, const double (&v)[K]) {
       double2* dst = const_cast<double2*>(slot_ptr(base, node, l));
 #pragma unroll
       for (int kp = 0; kp < K / 2; ++kp) __stcg(dst + kp * 32, make_double2(v[2 * kp], v[2 * kp + 1]));
+      if constexpr (K & 1) __stcg(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane, v[K - 1]);
     };
     // ---- staged operands (SOP): the next unit's operands are copied into a
     // per-warp shared stage with cp.async while this unit computes
@@ -273,13 +293,17 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
       double2* dst = reinterpret_cast<double2*>(opbuf(stage, which)) + lane;
 #pragma unroll
       for (int kp = 0; kp < K / 2; ++kp) cpa16(dst + kp * 32, src + kp * 32);
+      if constexpr (K & 1)
+        cpa8(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane,
+             reinterpret_cast<const double*>(src - lane + (K / 2) * 32) + lane);
       cpa4(xpbuf(stage, which) + lane, xsrc);
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
       const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
       double* dst = opbuf(stage, which);
 #pragma unroll
-      for (int ki = 0; ki < K; ++ki) cpa8(dst + ((ki >> 1) * 32 + lane) * 2 + (ki & 1), col + ki * 4);
+      for (int ki = 0; ki < K; ++ki)
+        cpa8(dst + (ki < 2 * (K / 2) ? ((ki >> 1) * 32 + lane) * 2 + (ki & 1) : (K / 2) * 64 + lane), col + ki * 4);
       xpbuf(stage, which)[lane] = 0;
     };
     auto read_op = [&](int stage, int which, double (&v)[K], int& x) {
@@ -290,6 +314,7 @@ __global__ void __launch_bounds__(128, (MP <= 32 ? 3 : 2)) walkm_kernel(const __
         v[2 * kp] = d.x;
         v[2 * kp + 1] = d.y;
       }
+      if constexpr (K & 1) v[K - 1] = reinterpret_cast<const double*>(src - lane + (K / 2) * 32)[lane];
       x = xpbuf(stage, which)[lane];
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
