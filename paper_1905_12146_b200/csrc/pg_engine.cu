@@ -492,8 +492,13 @@ struct pg_engine {
 
   void prepare_geometry() {
     use_walkm = m > 8 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
-    if (use_walkm) MP = m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
-    else MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
+    if (use_walkm) {
+      MP = m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
+      // walkm indexes its tables and per-warp scratch with 32-bit offsets
+      const int64_t lim = int64_t(1) << 31;
+      if (int64_t(B()) * L * (MP + A) * MP >= lim || int64_t(N) * L * MP * 32 >= lim) use_walkm = false;
+    }
+    if (!use_walkm) MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
     int nc4 = 0;
     const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;

@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   constexpr int WPC = Gm::WPC, CT = 32 * WPC;  // warps / threads per CTA
   const int warp = blockIdx.x * WPC + wib;
   const int ntile_cta = (p.P + 8 * WPC - 1) / (8 * WPC);
-  const size_t slotd = size_t(L) * K * 32;  // doubles per node slot per warp
+  // 32-bit element offsets inside the per-warp scratch and the K1 tables
+  // (the host guarantees they fit) keep the index math to one IMAD.WIDE
+  const int slotd = L * K * 32;  // doubles per node slot per warp
   double* E = p.escr + size_t(warp) * size_t(N - 1) * slotd;
   double* Qs = p.qscr + size_t(warp) * size_t(N - 1) * slotd;
   int* Ex = PM.eexp + size_t(warp) * size_t(N - 1) * L * 8;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
 
   // stage one (node, category) matrix in B-fragment order (contiguous copy)
   auto stage_P = [&](double* buf, const double* tab, int node, int l) {
-    const double* src = tab + (size_t(node - 1) * L + l) * size_t(FRAG);
+    const double* src = tab + ((node - 1) * L + l) * FRAG;
     for (int i = tid; i < FRAG / 2; i += CT) cpa16(buf + 2 * i, src + 2 * i);
   };
   // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     const int sc = valid ? s : p.P - 1;
     const double w = valid ? p.weights[sc] : 0.0;
     const uint8_t* codes = p.codes + sc;
-    const size_t Pc = size_t(p.Pc);
+    const int Pc = int(p.Pc);
     const int n = p.nsteps, U = n * L;
     const bool pf = PF && L > 1;  // (L == 1 would read a slot this unit is still writing)
     const bool sop = Gm::SOP && L > 1;
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
     // an odd last k-step as [lane] double
     auto slot_ptr = [&](const double* base, int node, int l) {
-      return reinterpret_cast<const double2*>(base + size_t(node - N - 1) * slotd + size_t(l) * K * 32) + lane;
+      return reinterpret_cast<const double2*>(base + ((node - N - 1) * slotd + l * (K * 32))) + lane;
     };
     auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
       const double2* src = slot_ptr(base, node, l);
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       cpa4(xpbuf(stage, which) + lane, xsrc);
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
-      const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+      const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
       double* dst = opbuf(stage, which);
 #pragma unroll
       for (int ki = 0; ki < K; ++ki)
@@ -318,18 +320,18 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       x = xpbuf(stage, which)[lane];
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
-      const double* col = p.tc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+      const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
 #pragma unroll
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
     // Q e of a tip = the same column of Q P (built by K1): a gather, not a mat-vec
     auto gather_q = [&](int node, int code, int l, double (&v)[K]) {
-      const double* col = p.qtc + ((size_t(node - 1) * L + l) * NC + code) * MP + t;
+      const double* col = p.qtc + (((node - 1) * L + l) * NC + code) * MP + t;
 #pragma unroll
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
-    auto exp_idx = [&](int node, int l) { return (size_t(node - N - 1) * L + l) * 8 + q; };
-    auto tipcode = [&](int node) -> int { return node <= N ? int(codes[size_t(node - 1) * Pc]) : 0; };
+    auto exp_idx = [&](int node, int l) { return ((node - N - 1) * L + l) * 8 + q; };
+    auto tipcode = [&](int node) -> int { return node <= N ? int(codes[int64_t(node - 1) * Pc]) : 0; };
     auto copyv = [&](double (&dst)[K], const double (&src)[K]) {
 #pragma unroll
       for (int ki = 0; ki < K; ++ki) dst[ki] = src[ki];
