@@ -1,14 +1,18 @@
 // K2 for large state spaces (m = 9..64: amino acids, codons) on the fp64
 // tensor cores (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind).
 //
-// Work unit: a CTA of 4 warps owns 32 patterns (8 per warp) and walks the
-// tree in lock-step, one (node, rate category) at a time, so each P(t) block
-// (MP x MP fp64) is staged once in shared memory and reused by all 32
-// patterns.  Every mat-vec  y^T = x^T M  over a warp's 8 patterns is a chain of
-// DMMA tiles: A = x^T (8 patterns x 4 states), B = 4 x 8 slice of M, D = y^T
-// (8 patterns x 8 states).  Vectors live in the A-fragment layout (pattern =
-// lane/4, states 4k + lane%4); the D fragments are converted back through a
-// per-warp shared buffer.
+// Work unit: a CTA of WPC warps (8 patterns per warp) walks the tree in
+// lock-step, one (node, rate category) at a time, so each P(t) block is
+// staged once in shared memory and reused by all of the CTA's patterns.
+// Every mat-vec  y^T = x^T M  over a warp's 8 patterns is a chain of DMMA
+// tiles: A = x^T (8 patterns x 4 states), B = 4 x 8 slice of M, D = y^T.
+// Vectors live in the A-fragment layout (pattern = lane/4, states 4k +
+// lane%4).  K1 writes P, P^T and Q in exact B-fragment order with the output
+// columns permuted (sigma(ni, g) = 4(2ni + g%2) + g/2) so that D tile ni holds
+// A-layout entries 2ni and 2ni+1: chained mat-vecs need no shuffles, staging
+// is a contiguous copy and shared-memory reads are conflict free.  With an
+// odd number of k-steps (20 states: K = 5) the last D entry is padding and
+// is dropped.
 //
 // Scaling: categories are processed one at a time, so each (pattern,
 // category) vector carries its own power-of-two exponent (stored beside the
