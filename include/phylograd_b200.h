@@ -159,13 +159,26 @@ int pg_newick_parse(const char* text, int* tip_count, int32_t* parent, int32_t* 
 /* alignment.hpp:186-229 from_codes compression, first-occurrence order.
  * codes [ntax][sites] int32 in -1..m-1 (validated).  Returns a handle and the
  * pattern count; pg_compress_result then writes pattern_codes [ntax][P]
- * (int32), weights[P] and, if non-NULL, site_to_pattern[sites].  Hashing is
+ * (int32), weights[P] and site_to_pattern[sites] (each skipped when NULL).  Hashing is
  * multithreaded; the output order is bit-exact with the reference's std::map
  * first-occurrence order. */
 int pg_compress_codes(int ntax, int64_t sites, const int32_t* codes, int state_count, void** handle,
                       int* pattern_count);
 int pg_compress_result(void* handle, int32_t* pattern_codes, int64_t* weights, int32_t* site_to_pattern);
 void pg_compress_free(void* handle);
+
+/* The same compression on the GPU (pg_compress.cu):
+ * codes int8 [ntax][sites] (host memory, or device memory on `device` when
+ * codes_on_device != 0), values -1..m-1.  Bit-exact with pg_compress_codes:
+ * first-occurrence pattern order, int64 weights, site -> pattern map; hash
+ * collisions are detected by a full column comparison and re-hashed.
+ * pg_compress_result_gpu copies the results to host arrays (any may be NULL)
+ * and reports the device time of the compression kernels. */
+int pg_compress_codes_gpu(int ntax, int64_t sites, const int8_t* codes, int codes_on_device, int state_count,
+                          int device, void** handle, int* pattern_count);
+int pg_compress_result_gpu(void* handle, int8_t* pattern_codes, int64_t* weights, int32_t* site_to_pattern,
+                           float* device_ms);
+void pg_compress_free_gpu(void* handle);
 
 /* Seeded synthetic workloads standing in for the paper's datasets
  * (BASELINE.json configs): Yule tree, model draws, forward

@@ -2,13 +2,13 @@
 log-likelihood gradient (arXiv 1905.12146), drop-in for the reference's
 LikelihoodEngine hot path.  See DESIGN.md."""
 from .api import (EngineOptions, GradientReport, LikelihoodEngine, RateCategories, RawAlignment,
-                  SitePatternAlignment, SubstitutionModel, Tree, branch_lengths_from_clock,
+                  SitePatternAlignment, SubstitutionModel, Tree, branch_lengths_from_clock, compress_codes_gpu,
                   discrete_gamma_categories, node_time_gradient, parse_fasta, parse_newick)
 from ._lib import (CudaFailure, InvalidArgument, LogicError, NewickError, NotSupported, PgError, RuntimeFailure)
 
 __all__ = [
     "EngineOptions", "GradientReport", "LikelihoodEngine", "RateCategories", "RawAlignment", "SitePatternAlignment",
-    "SubstitutionModel", "Tree", "branch_lengths_from_clock", "discrete_gamma_categories", "node_time_gradient",
+    "SubstitutionModel", "Tree", "branch_lengths_from_clock", "compress_codes_gpu", "discrete_gamma_categories", "node_time_gradient",
     "parse_fasta", "parse_newick", "CudaFailure", "InvalidArgument", "LogicError", "NewickError", "NotSupported",
     "PgError", "RuntimeFailure",
 ]

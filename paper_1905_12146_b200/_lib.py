@@ -37,7 +37,8 @@ EXPORTS = [
     "pg_evaluate_device", "pg_check_errors", "pg_set_stream", "pg_get_partials", "pg_get_site_log_likelihoods",
     "pg_node_visits", "pg_reset_node_visits", "pg_invalidate_caches", "pg_engine_info", "pg_last_walk_ms",
     "pg_timing", "pg_engine_variant",
-    "pg_newick_parse", "pg_compress_codes", "pg_compress_result", "pg_compress_free", "pg_discrete_gamma",
+    "pg_newick_parse", "pg_compress_codes", "pg_compress_result", "pg_compress_free", "pg_compress_codes_gpu",
+    "pg_compress_result_gpu", "pg_compress_free_gpu", "pg_discrete_gamma",
     "pg_synth_create", "pg_synth_tree", "pg_synth_model", "pg_synth_patterns", "pg_synth_free",
 ]
 
@@ -173,6 +174,9 @@ def _declare(L):
         "pg_compress_codes": (I, [I, C.c_int64, PI32, I, C.POINTER(P), C.POINTER(I)]),
         "pg_compress_result": (I, [P, PI32, PI64, PI32]),
         "pg_compress_free": (None, [P]),
+        "pg_compress_codes_gpu": (I, [I, C.c_int64, P, I, I, I, C.POINTER(P), C.POINTER(I)]),
+        "pg_compress_result_gpu": (I, [P, P, PI64, PI32, C.POINTER(C.c_float)]),
+        "pg_compress_free_gpu": (None, [P]),
         "pg_discrete_gamma": (I, [D, I, PD, PD]),
         "pg_synth_create": (I, [C.POINTER(SynthSpec), C.POINTER(P), C.POINTER(I), C.POINTER(I)]),
         "pg_synth_tree": (I, [P, PI32, PI32, PI32, PD, PD, PD]),

@@ -258,9 +258,13 @@ class SitePatternAlignment:
         return SitePatternAlignment(raw.taxa, 4, codes, weights, amb, columns, raw.site_count())
 
     @staticmethod
-    def from_codes(taxa: Sequence[str], codes, state_count: int) -> "SitePatternAlignment":
+    def from_codes(taxa: Sequence[str], codes, state_count: int, device=None) -> "SitePatternAlignment":
         """alignment.hpp:186-229 (first-occurrence order, bit-exact), compressed
-        by the multithreaded hash compressor in the C-ABI."""
+        by the multithreaded hash compressor in the C-ABI, or on GPU `device`
+        (pg_compress_codes_gpu) when given."""
+        if device is not None:
+            aln, _ = compress_codes_gpu(taxa, codes, state_count, device)
+            return aln
         if state_count < 2:
             raise InvalidArgument("alignment: state count must be >= 2")
         codes = i32(codes)
@@ -279,6 +283,39 @@ class SitePatternAlignment:
         finally:
             L.pg_compress_free(h)
         return SitePatternAlignment(taxa, state_count, pc.astype(np.int8), w, None, None, codes.shape[1])
+
+
+def compress_codes_gpu(taxa: Sequence[str], codes, state_count: int, device: int = 0, with_site_map=False):
+    """GPU first-occurrence compression (pg_compress_codes_gpu, SURVEY.md §8f
+    row 3), bit-exact with from_codes.  `codes` is int8-convertible [ntax][sites]
+    (values -1..m-1).  Returns (SitePatternAlignment, info) where info holds
+    the device time of the compression kernels and, if requested, the
+    site -> pattern map."""
+    if state_count < 2:
+        raise InvalidArgument("alignment: state count must be >= 2")
+    codes = np.asarray(codes)
+    if codes.ndim != 2 or codes.shape[0] != len(taxa):
+        raise InvalidArgument("alignment: taxa/codes mismatch")
+    if codes.size and (codes.min() < -1 or codes.max() >= state_count):
+        raise InvalidArgument("alignment: state code out of range")
+    c8 = np.ascontiguousarray(codes, dtype=np.int8)
+    L = lib()
+    h = C.c_void_p()
+    npat = C.c_int(0)
+    check(L.pg_compress_codes_gpu(c8.shape[0], c8.shape[1], c8.ctypes.data_as(C.c_void_p), 0, state_count, device,
+                                  C.byref(h), C.byref(npat)))
+    try:
+        P = npat.value
+        pc = np.zeros((c8.shape[0], P), np.int8)
+        w = np.zeros(P, np.int64)
+        site = np.zeros(c8.shape[1], np.int32) if with_site_map else None
+        ms = C.c_float(0.0)
+        check(L.pg_compress_result_gpu(h, pc.ctypes.data_as(C.c_void_p), ptr(w, C.c_int64),
+                                       ptr(site, C.c_int32) if site is not None else None, C.byref(ms)))
+    finally:
+        L.pg_compress_free_gpu(h)
+    info = {"device_ms": float(ms.value), "site_to_pattern": site}
+    return SitePatternAlignment(taxa, state_count, pc, w, None, None, c8.shape[1]), info
 
 
 # -------------------------------------------------------------------- models

@@ -793,11 +793,13 @@ int pg_compress_codes(int ntax, int64_t sites, const int32_t* codes, int state_c
 int pg_compress_result(void* handle, int32_t* pattern_codes, int64_t* weights, int32_t* site_to_pattern) {
   return guarded([&] {
     auto* h = static_cast<CompressHandle*>(handle);
-    const size_t P = h->c.rep.size();
-    for (int r = 0; r < h->ntax; ++r)
-      for (size_t p = 0; p < P; ++p)
-        pattern_codes[size_t(r) * P + p] = h->codes[size_t(r) * size_t(h->sites) + size_t(h->c.rep[p])];
-    std::copy(h->c.weights.begin(), h->c.weights.end(), weights);
+    const size_t P = h ? h->c.rep.size() : 0;
+    if (!h) throw std::invalid_argument("alignment: null compression handle");
+    if (pattern_codes)
+      for (int r = 0; r < h->ntax; ++r)
+        for (size_t p = 0; p < P; ++p)
+          pattern_codes[size_t(r) * P + p] = h->codes[size_t(r) * size_t(h->sites) + size_t(h->c.rep[p])];
+    if (weights) std::copy(h->c.weights.begin(), h->c.weights.end(), weights);
     if (site_to_pattern) std::copy(h->c.site_to_pattern.begin(), h->c.site_to_pattern.end(), site_to_pattern);
   });
 }
