@@ -136,8 +136,9 @@ void pg_reset_node_visits(pg_engine* e);
 void pg_invalidate_caches(pg_engine* e);
 
 /* Introspection for benchmarks: kernels launched by the last evaluation,
- * average device ms of the walk kernel over the last evaluation, the chosen
- * launch geometry. */
+ * average device ms of the walk kernel over the last evaluation, and the
+ * launch geometry that evaluation used (the geometry is chosen lazily at the
+ * first evaluation after a topology / pattern / model change). */
 int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states);
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms);
 /* Walk-kernel variant of the current geometry: 0 generic register-tiled

@@ -37,6 +37,14 @@ void* pg_walk_kernel_large(int MP, int LC);
 namespace pg {
 namespace {
 
+// tip column indices: states stay, class columns move from old_mp + a to new_mp + a
+__global__ void pg_recode_kernel(uint8_t* codes, int64_t n, int old_mp, int new_mp) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = codes[i];
+    if (c >= old_mp) codes[i] = uint8_t(c - old_mp + new_mp);
+  }
+}
+
 #define PG_CUDA(call)                                                                                  \
   do {                                                                                                 \
     cudaError_t e_ = (call);                                                                           \
@@ -115,6 +123,7 @@ struct pg_engine {
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
   bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
+  int codes_mp = 0;        // MP the device tip codes' class columns are encoded for
   int walkm_wpc = 4;       // warps per CTA in walkm
   DevBuf<int> d_eexp, d_qexp;
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
@@ -295,6 +304,7 @@ struct pg_engine {
     d_amb.upload(ambv.data(), ambv.size(), stream);
     PG_CUDA(cudaStreamSynchronize(stream));
     m_aln = mm;
+    codes_mp = mp;
     P = np;
     Pc = int64_t(std::max<int64_t>(pc, 32));
     A = na + 1;
@@ -500,6 +510,15 @@ struct pg_engine {
     }
     if (!use_walkm) MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
+    if (codes_mp != MP) {
+      // class columns (ambiguity / missing) were encoded as codes_mp + a at
+      // set_patterns; the chosen kernel pads the states to MP instead
+      const int64_t n = int64_t(N) * Pc;
+      pg_recode_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, stream>>>(d_codes.p, n, codes_mp,
+                                                                                            MP);
+      PG_CUDA(cudaGetLastError());
+      codes_mp = MP;
+    }
     int nc4 = 0;
     const int maxLC = MP == 4 ? 4 : MP == 8 ? 2 : 1;
     LC = std::min(maxLC, pow2ceil(L));

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   constexpr bool DUAL = MP <= 32;
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
+  constexpr bool DESC2 = MP > 32;
   extern __shared__ __align__(16) double smd[];
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
@@ -361,6 +362,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       };
       int4 stc = p.post[0];
       int4 stn = n > 1 ? p.post[1] : stc;
+      // large MP: descriptors run two steps ahead (no load-use stall at the
+      // step boundary; measured C5 412 -> 405 ms); small MP keeps the
+      // registers (C4 at the 128-register cap: 203 vs 213 ms)
+      int4 stn2 = DESC2 && n > 2 ? p.post[2] : stn;
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
       auto stage_post_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
@@ -451,9 +456,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           cc0 = cn0;
           cc1 = cn1;
           if (i + 1 < n) {
-            stn = p.post[i + 1];
+            stn = DESC2 ? stn2 : p.post[i + 1];
             cn0 = tipcode(stn.y);
             cn1 = tipcode(stn.z);
+            if (DESC2 && i + 2 < n) stn2 = p.post[i + 2];
           }
         }
       }
@@ -487,6 +493,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       };
       int4 stc = p.pre[0];
       int4 stn = n > 1 ? p.pre[1] : stc;
+      // large MP: descriptors run two steps ahead (no load-use stall at the
+      // step boundary; measured C5 412 -> 405 ms); small MP keeps the
+      // registers (C4 at the 128-register cap: 203 vs 213 ms)
+      int4 stn2 = DESC2 && n > 2 ? p.pre[2] : stn;
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
       auto stage_pre_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
@@ -653,9 +663,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           cc0 = cn0;
           cc1 = cn1;
           if (i + 1 < n) {
-            stn = p.pre[i + 1];
+            stn = DESC2 ? stn2 : p.pre[i + 1];
             cn0 = tipcode(stn.y);
             cn1 = tipcode(stn.z);
+            if (DESC2 && i + 2 < n) stn2 = p.pre[i + 2];
           }
         }
         l = l2;

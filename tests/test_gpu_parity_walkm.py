@@ -1,0 +1,147 @@
+"""GPU parity of every large-state (DMMA walkm) instantiation and of the
+engine routes, against the CPU oracle: MP = 16 / 20 (odd k-step chains) /
+24 / 32 / 64, one and many rate categories (operand staging on and off),
+per-branch generators (non-homogeneous Q, Padé path), ambiguous and missing
+tips, the likelihood-only route (engine.hpp:146-149) against the gradient
+route (test_engine.cpp:161: routes agree), and a traversal-order change
+(test_engine.cpp:185).  Tolerances: tests/helpers.py (1e-9 relative)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import assert_logl, assert_vec, oracle_for
+
+pytestmark = pytest.mark.gpu
+
+pg = pytest.importorskip("paper_1905_12146_b200")
+from paper_1905_12146_b200 import synth  # noqa: E402
+from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCategories,  # noqa: E402
+                                       SitePatternAlignment, SubstitutionModel, Tree)
+
+
+def _reversible(m, rng, conc=2.0):
+    pi = rng.dirichlet(np.ones(m) * conc)
+    s = rng.lognormal(0, 0.7, (m, m))
+    s = (s + s.T) / 2
+    q = s * pi[None, :]
+    np.fill_diagonal(q, 0)
+    np.fill_diagonal(q, -q.sum(1))
+    q /= -np.sum(pi * np.diag(q))
+    return q, pi
+
+
+def _general(m, rng):
+    q = rng.lognormal(0, 0.5, (m, m))
+    np.fill_diagonal(q, 0)
+    np.fill_diagonal(q, -q.sum(1))
+    return q
+
+
+def _pair(m, L, taxa, sites, seed, branch_q=(), gaps=0.0, post_order=None, **opts):
+    rng = np.random.default_rng(seed)
+    q, pi = _reversible(m, rng)
+    mo = O.Model(q, pi, True)
+    for br, g in branch_q:
+        mo.set_branch_generator(br, g)
+    r = O.Rng(seed)
+    tree_o = O.Tree.random(r, taxa, 0.03, 0.8)
+    rates, probs = O.discrete_gamma(0.5, L) if L > 1 else ([1.0], [1.0])
+    codes = O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, sites, seed + 1)
+    if gaps:
+        codes = np.where(rng.random(codes.shape) < gaps, -1, codes)
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    aln_o = O.Alignment.from_codes(codes, m, labels)
+    ref = O.Engine(tree_o, aln_o, mo, rates, probs, **opts)
+    po = tree_o.post_order if post_order is None else post_order(tree_o)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, po)
+    aln = SitePatternAlignment.from_codes(labels, codes, m)
+    model = SubstitutionModel(q, pi, True)
+    for br, g in branch_q:
+        model.set_branch_generator(br, g)
+    eng = LikelihoodEngine(tree, aln, model, RateCategories(np.asarray(rates), np.asarray(probs)),
+                           EngineOptions(force_rescaling=opts.get("force_rescaling", False)))
+    return eng, ref
+
+
+def _check(eng, ref, hess=True):
+    ll, g, h = ref.branch_gradient(hess)
+    rep = eng.branch_gradient(hess)
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    if hess:
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    return rep
+
+
+@pytest.mark.parametrize("m,L", [(9, 1), (12, 4), (16, 3), (17, 4), (19, 1), (20, 5), (21, 2), (24, 4), (25, 1),
+                                 (31, 4), (33, 2), (48, 4), (64, 1), (64, 3)])
+def test_walkm_instantiations(m, L):
+    eng, ref = _pair(m, L, 13, 300, 97 * m + L, gaps=0.05)
+    _check(eng, ref)
+    assert eng.info()["kernel"] == "walkm_kernel"  # geometry of the last evaluation
+
+
+@pytest.mark.parametrize("m", [20, 61])
+def test_walkm_per_branch_generators(m):
+    """Non-homogeneous Q (engine.hpp:384-394; substitution.hpp:131-143): Padé
+    P(t) per branch, generators read from global fragment tables, tip Q e
+    from Q_branch P columns."""
+    rng = np.random.default_rng(m)
+    bq = [(1, _general(m, rng)), (4, _general(m, rng)), (9, _general(m, rng))]
+    eng, ref = _pair(m, 4, 11, 200, 5 * m, branch_q=bq)
+    _check(eng, ref)
+
+
+@pytest.mark.parametrize("m", [4, 6, 20, 61])
+def test_likelihood_route_matches_gradient_route(m):
+    """logL-only evaluation (post pass, engine.hpp:146-149) equals the logL of
+    the gradient evaluation (test_engine.cpp:161 asks 1e-14)."""
+    eng, ref = _pair(m, 4, 15, 250, 3 * m + 1)
+    ll_only = eng.log_likelihood()
+    eng.invalidate_caches()
+    rep = eng.branch_gradient()
+    assert abs(ll_only - rep.log_likelihood) <= 1e-14 * abs(rep.log_likelihood)
+    assert_logl(ll_only, ref.log_likelihood())
+
+
+@pytest.mark.parametrize("m", [4, 20])
+def test_traversal_order_invariance(m):
+    """A different valid post-order for the same tree (test_engine.cpp:185)
+    gives the same results to 1e-12 (the engine schedules its own order)."""
+    def right_first(t):
+        order = []
+
+        def visit(k):
+            if k > t.tip_count:
+                a, b = t.children[k]
+                visit(b)
+                visit(a)
+            order.append(k)
+        visit(t.root)
+        return np.asarray(order, np.int32)
+
+    e1, ref = _pair(m, 4, 14, 200, 77 + m)
+    e2, _ = _pair(m, 4, 14, 200, 77 + m, post_order=right_first)
+    r1, r2 = e1.branch_gradient(True), e2.branch_gradient(True)
+    assert abs(r1.log_likelihood - r2.log_likelihood) <= 1e-12 * abs(r1.log_likelihood)
+    assert np.allclose(r1.branch_gradient, r2.branch_gradient, rtol=1e-12, atol=1e-12 * np.abs(r1.branch_gradient).max())
+    _check(e1, ref)
+
+
+def test_walkm_forced_rescaling_neutral():  # test_engine.cpp:324-340 on the DMMA kernel
+    eng, ref = _pair(20, 4, 12, 150, 404, force_rescaling=True)
+    _check(eng, ref)
+
+
+def test_walkm_many_tiles_and_ragged_tail():
+    """Pattern counts that are not multiples of the 32-pattern CTA tile, at a
+    size that runs several tiles per CTA."""
+    for sites in (33, 1001):
+        inst = synth.generate("C4", sites=sites)
+        eng = synth.engine_for(inst)
+        ref = oracle_for(inst, blocks=4)
+        ll, g, _ = ref.branch_gradient(False)
+        rep = eng.branch_gradient()
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
