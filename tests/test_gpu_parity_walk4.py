@@ -1,0 +1,110 @@
+"""Direct oracle parity of every walk4_kernel<HOMOG, HESS, NC, LCV> variant
+(the C2/C3 bench kernel): pattern counts large enough that the engine picks
+walk4, one lane per pattern (LCV=4, the C3 geometry) and two (LCV=2, the C2
+geometry) forced through PG_WALK4_LCV, homogeneous and per-branch
+generators, with and without the Hessian, gaps only (NC=5) and IUPAC
+ambiguity classes (NC=16)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import assert_logl, assert_vec
+
+pytestmark = pytest.mark.gpu
+
+pg = pytest.importorskip("paper_1905_12146_b200")
+from paper_1905_12146_b200 import synth  # noqa: E402
+from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCategories,  # noqa: E402
+                                       SitePatternAlignment, SubstitutionModel, Tree, parse_fasta, parse_newick)
+
+
+@pytest.fixture(params=[4, 2], ids=["lcv4", "lcv2"])
+def lcv(request, monkeypatch):
+    monkeypatch.setenv("PG_WALK4_LCV", str(request.param))
+    return request.param
+
+
+def _branch_q(seed, B, k=5):
+    rng = np.random.default_rng(seed)
+    out = []
+    for br in rng.choice(np.arange(1, B + 1), size=k, replace=False):
+        q = rng.lognormal(0, 0.6, (4, 4))
+        np.fill_diagonal(q, 0)
+        np.fill_diagonal(q, -q.sum(1))
+        out.append((int(br), q))
+    return out
+
+
+def _instance_pair(inst, branch_q=()):
+    labels = inst.labels()
+    tree = Tree(inst.tip_count, inst.parent, inst.children, np.concatenate([[0.0], inst.branch_lengths, [0.0]]),
+                labels, inst.post_order)
+    aln = SitePatternAlignment(labels[1:inst.tip_count + 1], inst.states, inst.codes, inst.weights)
+    model = SubstitutionModel(inst.q, inst.pi, inst.reversible)
+    for br, q in branch_q:
+        model.set_branch_generator(br, q)
+    eng = LikelihoodEngine(tree, aln, model, RateCategories(inst.cat_rates, inst.cat_probs), EngineOptions())
+    tree_o = O.Tree.from_arrays(inst.tip_count, inst.parent, inst.children, inst.branch_lengths, inst.post_order)
+    aln_o = O.Alignment.from_patterns(inst.codes.astype(np.int32), inst.states, inst.weights)
+    model_o = O.Model(inst.q, inst.pi, inst.reversible)
+    for br, q in branch_q:
+        model_o.set_branch_generator(br, q)
+    ref = O.Engine(tree_o, aln_o, model_o, inst.cat_rates, inst.cat_probs, blocks=16)
+    ref._keep = (tree_o, aln_o, model_o)
+    return eng, ref
+
+
+@pytest.mark.parametrize("homog", [True, False], ids=["homog", "per_branch_q"])
+@pytest.mark.parametrize("hess", [False, True], ids=["grad", "hess"])
+def test_walk4_variants_c3_shape(lcv, homog, hess):
+    # C3 model family (raw non-reversible Q, Pade P(t)) on a 256-taxon Yule tree
+    inst = synth.generate("C3", sites=40000, tips=256)
+    bq = () if homog else _branch_q(3, inst.branches)
+    eng, ref = _instance_pair(inst, bq)
+    ll, g, h = ref.branch_gradient(hess)
+    rep = eng.branch_gradient(hess)
+    assert eng.info()["kernel"] == "walk4_kernel"
+    assert eng.info()["lanes_per_pattern"] == 4 // lcv
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    if hess:
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+
+
+def test_walk4_gaps_c2_shape(lcv):
+    inst = synth.generate("C2", sites=12000)  # GTR + 2 % gaps
+    eng, ref = _instance_pair(inst)
+    ll, g, _ = ref.branch_gradient(False)
+    rep = eng.branch_gradient()
+    assert eng.info()["kernel"] == "walk4_kernel"
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+
+
+def test_walk4_iupac_classes(lcv):
+    """IUPAC ambiguity classes (alignment.hpp:50-70) widen the TC table to
+    NC = 16 columns."""
+    rng = np.random.default_rng(8)
+    taxa, sites = 24, 9000
+    alphabet = np.array(list("ACGT"))
+    amb = np.array(list("RYKMSWBDHVN-?"))
+    cols = alphabet[rng.integers(0, 4, size=(taxa, sites))]
+    mask = rng.random((taxa, sites)) < 0.08
+    cols = np.where(mask, amb[rng.integers(0, amb.size, size=(taxa, sites))], cols)
+    tree_o = O.Tree.random(O.Rng(4), taxa, 0.02, 0.3)
+    names = [tree_o.labels[k] for k in range(1, taxa + 1)]
+    fasta = "".join(f">{names[i]}\n{''.join(cols[i])}\n" for i in range(taxa))
+    newick = tree_o.serialize()
+    model = SubstitutionModel.hky85(2.0, [0.3, 0.2, 0.2, 0.3])
+    cats = pg.discrete_gamma_categories(0.5, 4)
+    tree = parse_newick(newick)
+    aln = SitePatternAlignment.compress(parse_fasta(fasta))
+    eng = LikelihoodEngine(tree, aln, model, cats, EngineOptions())
+    ref = O.Engine(O.Tree.parse(newick), O.Alignment.from_fasta(fasta), O.Model.hky85(2.0, [0.3, 0.2, 0.2, 0.3]),
+                   list(cats.rates), list(cats.probs), blocks=8)
+    ll, g, h = ref.branch_gradient(True)
+    rep = eng.branch_gradient(True)
+    assert eng.info()["kernel"] == "walk4_kernel"
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")

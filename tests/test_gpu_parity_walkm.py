@@ -145,3 +145,27 @@ def test_walkm_many_tiles_and_ragged_tail():
         rep = eng.branch_gradient()
         assert_logl(rep.log_likelihood, ll)
         assert_vec(rep.branch_gradient, g)
+
+
+@pytest.mark.parametrize("m,L", [(2, 1), (3, 2), (4, 1), (4, 4), (4, 8), (5, 4), (8, 2), (20, 4), (61, 2)])
+def test_gaps_every_kernel(m, L):
+    """Missing data (code -1 -> all-ones class column, alignment.hpp:223-224)
+    through every kernel family: generic walk_kernel, walk4, walkm."""
+    eng, ref = _pair(m, L, 10, 220, 1234 + 10 * m + L, gaps=0.15)
+    _check(eng, ref)
+
+
+@pytest.mark.parametrize("m,L", [(4, 4), (4, 1), (20, 4), (61, 4)])
+@pytest.mark.parametrize("taxa", [2, 3])
+def test_smallest_trees(m, L, taxa):
+    """Two- and three-taxon trees (a root-only schedule; test_engine.cpp:24-35)."""
+    eng, ref = _pair(m, L, taxa, 40, 55 + taxa * m + L, gaps=0.1)
+    _check(eng, ref)
+
+
+@pytest.mark.parametrize("m,L", [(4, 4), (6, 2), (20, 4), (61, 1)])
+@pytest.mark.parametrize("sites", [1, 5])
+def test_single_and_few_patterns(m, L, sites):
+    """P smaller than one warp / CTA tile (every lane but a few idle)."""
+    eng, ref = _pair(m, L, 9, sites, 700 + m + sites)
+    _check(eng, ref)
