@@ -110,9 +110,13 @@ struct WalkMGeom {
   static constexpr int FRAG = K * NT * 32;  // doubles of one matrix in B-fragment order
   // small state spaces double-buffer the P(t) blocks across units and stage
   // the next unit's operands in shared memory (SOP)
+#ifdef PG_WALKM_NOPIPE
+  static constexpr bool PIPE = false;
+#else
   static constexpr bool PIPE = MP <= 32;
+#endif
   static constexpr int NPB = PIPE ? 4 : 2;
-  static constexpr bool SOP = MP <= 32;
+  static constexpr bool SOP = PIPE;
   // warps per CTA (lock-step group sharing each staged matrix).  Measured on
   // C5: 8 warps with double-buffered 32 KB codon blocks (one CTA per SM) is
   // slower than two 4-warp CTAs (432 vs 423 ms).
@@ -132,10 +136,18 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // resident CTA), kept selectable
   constexpr bool PF = false;
   // interleave the two children's mat-vecs (small state spaces: short chains)
+#ifdef PG_WALKM_NODUAL
+  constexpr bool DUAL = false;
+#else
   constexpr bool DUAL = MP <= 32;
+#endif
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
+#ifndef PG_WALKM_DESC2
   constexpr bool DESC2 = MP > 32;
+#else
+  constexpr bool DESC2 = PG_WALKM_DESC2;
+#endif
   extern __shared__ __align__(16) double smd[];
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
@@ -631,14 +643,17 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           matvec2(pbuf(0, par), ta, qa_, pbuf(1, par), tb, qb_, false);
           emit_q(ca, qa_, xq + xb);
           emit_q(cb, qb_, xq + xa);
-        } else if (a_int) {
-          double qo[K];
-          matvec_PT(pbuf(0, par), ta, qo);
-          emit_q(ca, qo, xq + xb);
-        } else if (b_int) {
-          double qo[K];
-          matvec_PT(pbuf(1, par), tb, qo);
-          emit_q(cb, qo, xq + xa);
+        } else {
+          if (a_int) {
+            double qo[K];
+            matvec_PT(pbuf(0, par), ta, qo);
+            emit_q(ca, qo, xq + xb);
+          }
+          if (b_int) {
+            double qo[K];
+            matvec_PT(pbuf(1, par), tb, qo);
+            emit_q(cb, qo, xq + xa);
+          }
         }
         if (step_end) {
           const double inv = 1.0 / mix.v[0];

@@ -21,6 +21,7 @@ def oracle_for(inst, blocks=1, **opts):
 
 
 def assert_logl(a, b, rtol=RTOL):
+    assert np.isfinite(a), f"logL {a!r} is not finite"
     assert abs(a - b) <= rtol * max(abs(b), 1e-300), f"logL {a!r} vs oracle {b!r} (rel {abs(a - b) / abs(b):.3e})"
 
 
@@ -28,10 +29,12 @@ def assert_vec(a, b, rtol=RTOL, what="gradient"):
     a = np.asarray(a)
     b = np.asarray(b)
     assert a.shape == b.shape
+    assert np.all(np.isfinite(a)), f"{what}: {int(np.sum(~np.isfinite(a)))} non-finite components"
+    assert np.all(np.isfinite(b)), f"{what} (oracle): non-finite components"
     scale = np.max(np.abs(b)) if b.size else 0.0
     err = np.abs(a - b)
     tol = rtol * np.abs(b) + ATOL_REL_SCALE * scale
-    bad = np.nonzero(err > tol)[0]
+    bad = np.nonzero(~(err <= tol))[0]
     assert bad.size == 0, (f"{what}: {bad.size} components off; worst idx {bad[np.argmax(err[bad])]} "
                            f"got {a[bad[0]]!r} want {b[bad[0]]!r}; max rel {np.max(err / np.maximum(np.abs(b), 1e-300)):.3e}")
 
