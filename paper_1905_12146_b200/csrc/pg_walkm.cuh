@@ -135,11 +135,13 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // measured slower (C4 323 vs 236 ms: 168 registers + spills cost a
   // resident CTA), kept selectable
   constexpr bool PF = false;
-  // interleave the two children's mat-vecs (small state spaces: short chains)
-#ifdef PG_WALKM_NODUAL
-  constexpr bool DUAL = false;
+  // interleaving the two children's mat-vecs (dmma_chain2) was a win at 168
+  // registers / 3 CTAs per SM; at the 128-register cap of 4 CTAs it spills
+  // (measured C4 179 ms without vs 202 ms with; C5 436 vs 511 ms)
+#ifdef PG_WALKM_DUAL
+  constexpr bool DUAL = true;
 #else
-  constexpr bool DUAL = MP <= 32;
+  constexpr bool DUAL = false;
 #endif
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
