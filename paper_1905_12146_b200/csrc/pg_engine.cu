@@ -26,7 +26,7 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv) {
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
 }
 int pg_walk4_nc(int nc);
-void* pg_walkm_kernel(int mp);
+void* pg_walkm_kernel(int mp, bool hess);
 size_t pg_walkm_smem(int mp);
 int pg_walkm_wpc(int mp);
 
@@ -740,9 +740,13 @@ void* select_walk(int MP, int LC) {
 int pg_engine::walk_max_blocks_per_sm() {
   int nb = 0;
   if (use_walkm) {
-    const void* fn = pg_walkm_kernel(MP);
-    PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 * walkm_wpc, walk_smem));
+    for (int h = 0; h < 2; ++h) {
+      const void* fn = pg_walkm_kernel(MP, h != 0);
+      PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
+      int b = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * walkm_wpc, walk_smem));
+      nb = h == 0 ? b : std::min(nb, b);
+    }
     return std::max(nb, 1);
   }
   if (use_walk4) {
@@ -837,7 +841,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     pm.fpt = d_fpt.p;
     pm.fq = d_fq.p;
     pm.homogeneous = branch_q.empty() ? 1 : 0;
-    void* fn = pg_walkm_kernel(MP);
+    void* fn = pg_walkm_kernel(MP, do_hess);
     void* args[] = {&pm};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / walkm_wpc)), dim3(32 * walkm_wpc), args, walk_smem, stream));
     return;

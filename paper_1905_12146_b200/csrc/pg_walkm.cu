@@ -1,12 +1,18 @@
 // Instantiations of the DMMA large-state walk kernel (pg_walkm.cuh).
 #include "pg_walkm.cuh"
 
-void* pg_walkm_kernel(int mp) {
-  if (mp == 16) return reinterpret_cast<void*>(&pgk::walkm_kernel<16>);
-  if (mp == 20) return reinterpret_cast<void*>(&pgk::walkm_kernel<20>);
-  if (mp == 24) return reinterpret_cast<void*>(&pgk::walkm_kernel<24>);
-  if (mp == 32) return reinterpret_cast<void*>(&pgk::walkm_kernel<32>);
-  if (mp == 64) return reinterpret_cast<void*>(&pgk::walkm_kernel<64>);
+template <int MP>
+static void* pick(bool hess) {
+  return hess ? reinterpret_cast<void*>(&pgk::walkm_kernel<MP, true>)
+              : reinterpret_cast<void*>(&pgk::walkm_kernel<MP, false>);
+}
+
+void* pg_walkm_kernel(int mp, bool hess) {
+  if (mp == 16) return pick<16>(hess);
+  if (mp == 20) return pick<20>(hess);
+  if (mp == 24) return pick<24>(hess);
+  if (mp == 32) return pick<32>(hess);
+  if (mp == 64) return pick<64>(hess);
   return nullptr;
 }
 

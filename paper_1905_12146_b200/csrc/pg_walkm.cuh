@@ -53,7 +53,9 @@ __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all
 // flight to cover the tensor-pipe latency.
 template <int K, int NT, class F>
 __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT][2], F bfrag) {
-  constexpr int NSPLIT = NT < 8 ? 2 : 1;
+  // one accumulator chain per n-tile: at the 128-register cap the even/odd
+  // k-step split costs more than it hides (C4 176 vs 179 ms)
+  constexpr int NSPLIT = 1;
   double acc[NSPLIT][NT][2];
 #pragma unroll
   for (int h = 0; h < NSPLIT; ++h)
@@ -127,7 +129,9 @@ struct WalkMGeom {
   static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD) * sizeof(double); }
 };
 
-template <int MP>
+// HESS: Hessian-diagonal variant (a template parameter so the gradient-only
+// kernel does not carry the Q^2 e terms in its register allocation)
+template <int MP, bool HESS>
 __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_MINB_SMALL : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
@@ -260,8 +264,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     return e >= -1074 ? ldexp(1.0, e) : 0.0;
   };
   // running mixture over categories with exponents: value = acc * 2^ref
+  constexpr int NR = HESS ? 5 : 3;  // mixture terms: den, num_a, num_b (, num2_a, num2_b)
   struct Mix {
-    double v[5];
+    double v[NR];
     int ref;
   };
 
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       double an[K], bn[K];
       int xan = 0, xbn = 0;
       if (pf) load_post(stc, cc0, cc1, 0, an, bn, xan, xbn);
-      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      Mix mix{{}, INT_MIN};
       int i = 0, l = 0;
       for (int u = 0; u < U; ++u) {
         const int par = PIPE ? (u & 1) : 0;
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         l = l2;
         if (step_end) {
           ++i;
-          mix = Mix{{0, 0, 0, 0, 0}, INT_MIN};
+          mix = Mix{{}, INT_MIN};
           stc = stn;
           cc0 = cn0;
           cc1 = cn1;
@@ -527,7 +532,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       int xqn = 0, xan = 0, xbn = 0;
       if (pf) load_pre(stc, cc0, cc1, 0, qn, ean, ebn, xqn, xan, xbn);
       // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
-      Mix mix{{0, 0, 0, 0, 0}, INT_MIN};
+      Mix mix{{}, INT_MIN};
       int i = 0, l = 0;
       for (int u = 0; u < U; ++u) {
         const int par = PIPE ? (u & 1) : 0;
@@ -581,9 +586,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           dd = fma(ta[ki], ea[ki], dd);
         }
         const double wl = p.probs[l], cl = p.rates[l];
-        double term[5];
+        double term[NR];
         term[0] = wl * quad_sum(dd);
-        term[3] = term[4] = 0.0;
         {
           double ua[K], ub[K];
           if (DUAL && a_int && b_int) {
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           }
           term[1] = cl * wl * quad_sum(d1a);
           term[2] = cl * wl * quad_sum(d1b);
-          if (p.hess) {
+          if constexpr (HESS) {
             double u2a[K], u2b[K];
             if (DUAL) {
               matvec2(homog ? Qsm : Qa, ua, u2a, homog ? Qsm : Qb, ub, u2b, !homog);
@@ -623,12 +627,12 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (El > mix.ref) {
           if (mix.ref != INT_MIN) {
             const double down = pow2(mix.ref - El);
-            for (int r = 0; r < 5; ++r) mix.v[r] *= down;
+            for (int r = 0; r < NR; ++r) mix.v[r] *= down;
           }
           mix.ref = El;
         }
         const double scl = pow2(El - mix.ref);
-        for (int r = 0; r < 5; ++r) mix.v[r] = fma(term[r], scl, mix.v[r]);
+        for (int r = 0; r < NR; ++r) mix.v[r] = fma(term[r], scl, mix.v[r]);
         // outgoing pre-partials of internal children: q_x = P_x^T top
         if (!PIPE && (a_int || b_int)) {
           cpa_wait_all();
@@ -666,7 +670,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
             atomicAdd(Acc + ca, ga);
             atomicAdd(Acc + cb, gb);
           }
-          if (p.hess) {
+          if constexpr (HESS) {
             const double ha = warp_sum(owner ? w * (mix.v[3] * inv - r1a * r1a) : 0.0);
             const double hb = warp_sum(owner ? w * (mix.v[4] * inv - r1b * r1b) : 0.0);
             if (lane == 0) {
@@ -675,7 +679,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
             }
           }
           ++i;
-          mix = Mix{{0, 0, 0, 0, 0}, INT_MIN};
+          mix = Mix{{}, INT_MIN};
           stc = stn;
           cc0 = cn0;
           cc1 = cn1;
