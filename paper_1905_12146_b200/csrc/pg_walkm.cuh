@@ -76,24 +76,6 @@ __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT]
   }
 }
 
-// Two independent chains interleaved (the two children of a pre-order step):
-// twice the DMMAs in flight; a shared B operand is loaded once.
-template <int K, int NT, class FA, class FB>
-__device__ __forceinline__ void dmma_chain2(const double (&xa)[K], double (&da)[NT][2], FA fa, const double (&xb)[K],
-                                            double (&db)[NT][2], FB fb, bool shared_b) {
-#pragma unroll
-  for (int ni = 0; ni < NT; ++ni) da[ni][0] = da[ni][1] = db[ni][0] = db[ni][1] = 0.0;
-#pragma unroll
-  for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      const double ba = fa(ki, ni);
-      const double bb = shared_b ? ba : fb(ki, ni);
-      dmma(da[ni][0], da[ni][1], xa[ki], ba);
-      dmma(db[ni][0], db[ni][1], xb[ki], bb);
-    }
-}
-
 // Resident CTAs per SM for MP <= 32: 4 caps registers at 128 (C4: 204 ms vs
 // 211 ms at 3 CTAs / 168 registers).
 #ifndef PG_WALKM_MINB_SMALL
@@ -112,11 +94,7 @@ struct WalkMGeom {
   static constexpr int FRAG = K * NT * 32;  // doubles of one matrix in B-fragment order
   // small state spaces double-buffer the P(t) blocks across units and stage
   // the next unit's operands in shared memory (SOP)
-#ifdef PG_WALKM_NOPIPE
-  static constexpr bool PIPE = false;
-#else
   static constexpr bool PIPE = MP <= 32;
-#endif
   static constexpr int NPB = PIPE ? 4 : 2;
   static constexpr bool SOP = PIPE;
   // warps per CTA (lock-step group sharing each staged matrix).  Measured on
@@ -135,25 +113,12 @@ template <int MP, bool HESS>
 __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_MINB_SMALL : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
-  // operand prefetch into registers for the next (step, category) unit:
-  // measured slower (C4 323 vs 236 ms: 168 registers + spills cost a
-  // resident CTA), kept selectable
-  constexpr bool PF = false;
-  // interleaving the two children's mat-vecs (dmma_chain2) was a win at 168
-  // registers / 3 CTAs per SM; at the 128-register cap of 4 CTAs it spills
-  // (measured C4 179 ms without vs 202 ms with; C5 436 vs 511 ms)
-#ifdef PG_WALKM_DUAL
-  constexpr bool DUAL = true;
-#else
-  constexpr bool DUAL = false;
-#endif
+  // (measured and removed: register prefetch of the next unit's operands,
+  // interleaved mat-vecs of the two children -- both cost registers at the
+  // 128-register cap of 4 CTAs per SM)
   const WalkParams& p = PM.p;
   constexpr bool PIPE = Gm::PIPE;
-#ifndef PG_WALKM_DESC2
-  constexpr bool DESC2 = MP > 32;
-#else
-  constexpr bool DESC2 = PG_WALKM_DESC2;
-#endif
+  constexpr bool DESC2 = MP > 32;  // step descriptors two ahead (see below)
   extern __shared__ __align__(16) double smd[];
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
@@ -207,21 +172,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       y[2 * ni] = d[ni][0];
       if (2 * ni + 1 < K) y[2 * ni + 1] = d[ni][1];
     }
-  };
-  // two mat-vecs with smem (or, if g, global) fragments, interleaved
-  auto matvec2 = [&](const double* fa, const double (&xa)[K], double (&ya)[K], const double* fb,
-                     const double (&xb)[K], double (&yb)[K], bool g) {
-    double da[NT][2], db[NT][2];
-    if (g)
-      dmma_chain2<K, NT>(
-          xa, da, [&](int ki, int ni) { return __ldg(fa + (ki * NT + ni) * 32 + lane); }, xb, db,
-          [&](int ki, int ni) { return __ldg(fb + (ki * NT + ni) * 32 + lane); }, fa == fb);
-    else
-      dmma_chain2<K, NT>(
-          xa, da, [&](int ki, int ni) { return fa[(ki * NT + ni) * 32 + lane]; }, xb, db,
-          [&](int ki, int ni) { return fb[(ki * NT + ni) * 32 + lane]; }, fa == fb);
-    unpack(da, ya);
-    unpack(db, yb);
   };
   auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
   auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
@@ -284,7 +234,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     const uint8_t* codes = p.codes + sc;
     const int Pc = int(p.Pc);
     const int n = p.nsteps, U = n * L;
-    const bool pf = PF && L > 1;  // (L == 1 would read a slot this unit is still writing)
     const bool sop = Gm::SOP && L > 1;
 
     // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
@@ -356,15 +305,11 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     };
     auto exp_idx = [&](int node, int l) { return ((node - N - 1) * L + l) * 8 + q; };
     auto tipcode = [&](int node) -> int { return node <= N ? int(codes[int64_t(node - 1) * Pc]) : 0; };
-    auto copyv = [&](double (&dst)[K], const double (&src)[K]) {
-#pragma unroll
-      for (int ki = 0; ki < K; ++ki) dst[ki] = src[ki];
-    };
 
     // ------------------------------------------------ post-order pass (a)
     // Units (step i, category l) in lock-step.  PIPE: the next unit's P(t)
-    // block is staged into the other buffer parity while this unit computes;
-    // PF: its operands are loaded into registers as well.
+    // block (and, with SOP, its operands) is staged into the other buffer
+    // parity while this unit computes.
     {
       auto load_post = [&](const int4 st, int c0, int c1, int l, double (&a)[K], double (&b)[K], int& xa, int& xb) {
         xa = xb = 0;
@@ -396,9 +341,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0);
       if (sop) stage_post_ops(stc, cc0, cc1, 0, 0);
       cpa_commit();
-      double an[K], bn[K];
-      int xan = 0, xbn = 0;
-      if (pf) load_post(stc, cc0, cc1, 0, an, bn, xan, xbn);
       Mix mix{{}, INT_MIN};
       int i = 0, l = 0;
       for (int u = 0; u < U; ++u) {
@@ -422,12 +364,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (sop) {
           read_op(u & 1, 0, a, xa);
           read_op(u & 1, 1, b, xb);
-        } else if (pf) {
-          copyv(a, an);
-          copyv(b, bn);
-          xa = xan;
-          xb = xbn;
-          if (has_next) load_post(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, an, bn, xan, xbn);
         } else {
           load_post(stc, cc0, cc1, l, a, b, xa, xb);
         }
@@ -528,9 +464,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       if (PIPE) stage_pre(stc, 0, 0);
       if (sop) stage_pre_ops(stc, cc0, cc1, 0, 0);
       cpa_commit();
-      double qn[K], ean[K], ebn[K];
-      int xqn = 0, xan = 0, xbn = 0;
-      if (pf) load_pre(stc, cc0, cc1, 0, qn, ean, ebn, xqn, xan, xbn);
       // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
       Mix mix{{}, INT_MIN};
       int i = 0, l = 0;
@@ -563,15 +496,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           }
           read_op(u & 1, 0, ea, xa);
           read_op(u & 1, 1, eb, xb);
-        } else if (pf) {
-          copyv(qv, qn);
-          copyv(ea, ean);
-          copyv(eb, ebn);
-          xq = xqn;
-          xa = xan;
-          xb = xbn;
-          if (has_next)
-            load_pre(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, qn, ean, ebn, xqn, xan, xbn);
         } else {
           load_pre(stc, cc0, cc1, l, qv, ea, eb, xq, xa, xb);
         }
@@ -590,14 +514,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         term[0] = wl * quad_sum(dd);
         {
           double ua[K], ub[K];
-          if (DUAL && a_int && b_int) {
-            matvec2(homog ? Qsm : Qa, ea, ua, homog ? Qsm : Qb, eb, ub, !homog);
-          } else {
-            if (a_int) matvec_Q(Qa, ea, ua);
-            else gather_q(ca, cc0, l, ua);
-            if (b_int) matvec_Q(Qb, eb, ub);
-            else gather_q(cb, cc1, l, ub);
-          }
+          if (a_int) matvec_Q(Qa, ea, ua);
+          else gather_q(ca, cc0, l, ua);
+          if (b_int) matvec_Q(Qb, eb, ub);
+          else gather_q(cb, cc1, l, ub);
           double d1a = 0.0, d1b = 0.0;
 #pragma unroll
           for (int ki = 0; ki < K; ++ki) {
@@ -608,12 +528,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           term[2] = cl * wl * quad_sum(d1b);
           if constexpr (HESS) {
             double u2a[K], u2b[K];
-            if (DUAL) {
-              matvec2(homog ? Qsm : Qa, ua, u2a, homog ? Qsm : Qb, ub, u2b, !homog);
-            } else {
-              matvec_Q(Qa, ua, u2a);
-              matvec_Q(Qb, ub, u2b);
-            }
+            matvec_Q(Qa, ua, u2a);
+            matvec_Q(Qb, ub, u2b);
             double d2a = 0.0, d2b = 0.0;
 #pragma unroll
             for (int ki = 0; ki < K; ++ki) {
@@ -644,22 +560,15 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           store_slot(Qs, x, l, qo);
           if (t == 0) Qx[exp_idx(x, l)] = xbase + ex;
         };
-        if (DUAL && a_int && b_int) {
-          double qa_[K], qb_[K];
-          matvec2(pbuf(0, par), ta, qa_, pbuf(1, par), tb, qb_, false);
-          emit_q(ca, qa_, xq + xb);
-          emit_q(cb, qb_, xq + xa);
-        } else {
-          if (a_int) {
-            double qo[K];
-            matvec_PT(pbuf(0, par), ta, qo);
-            emit_q(ca, qo, xq + xb);
-          }
-          if (b_int) {
-            double qo[K];
-            matvec_PT(pbuf(1, par), tb, qo);
-            emit_q(cb, qo, xq + xa);
-          }
+        if (a_int) {
+          double qo[K];
+          matvec_PT(pbuf(0, par), ta, qo);
+          emit_q(ca, qo, xq + xb);
+        }
+        if (b_int) {
+          double qo[K];
+          matvec_PT(pbuf(1, par), tb, qo);
+          emit_q(cb, qo, xq + xa);
         }
         if (step_end) {
           const double inv = 1.0 / mix.v[0];
