@@ -169,3 +169,35 @@ def test_single_and_few_patterns(m, L, sites):
     """P smaller than one warp / CTA tile (every lane but a few idle)."""
     eng, ref = _pair(m, L, 9, sites, 700 + m + sites)
     _check(eng, ref)
+
+
+def _caterpillar_pair(m, L, tips, sites, seed, blen, **opts):
+    rng = np.random.default_rng(seed)
+    q, pi = _reversible(m, rng)
+    mo = O.Model(q, pi, True)
+    tree_o = O.Tree.caterpillar(tips, blen)
+    rates, probs = O.discrete_gamma(0.5, L) if L > 1 else ([1.0], [1.0])
+    codes = O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, sites, seed + 1)
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    ref = O.Engine(tree_o, O.Alignment.from_codes(codes, m, labels), mo, rates, probs)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, tree_o.post_order)
+    eng = LikelihoodEngine(tree, SitePatternAlignment.from_codes(labels, codes, m), SubstitutionModel(q, pi, True),
+                           RateCategories(np.asarray(rates), np.asarray(probs)), EngineOptions(**opts))
+    return eng, ref
+
+
+@pytest.mark.parametrize("m,L,tips,sites", [(20, 4, 400, 24), (61, 2, 300, 12), (4, 4, 700, 6000)])
+def test_deep_caterpillar_rescaling(m, L, tips, sites):
+    """Caterpillars whose site likelihoods underflow double precision without
+    rescaling (test_engine.cpp:341-361) through walkm (20, 61 states) and
+    walk4 (4 states, enough patterns for the pipelined kernel)."""
+    eng, ref = _caterpillar_pair(m, L, tips, sites, 31 + m, 0.3)
+    ll, g, _ = ref.branch_gradient(False)
+    assert ll / max(1, sites) < -700.0 or ll < -5000.0  # far below the double range per site
+    rep = eng.branch_gradient()
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    off, _ = _caterpillar_pair(m, L, tips, sites, 31 + m, 0.3, disable_rescaling=True)
+    with pytest.raises(pg.RuntimeFailure, match="underflow"):
+        off.log_likelihood()
