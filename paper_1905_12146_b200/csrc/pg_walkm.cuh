@@ -46,6 +46,30 @@ __device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// mbarrier + 1-D bulk copy (TMA engine) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(mb))
+      : "memory");
+}
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // D (8 patterns x 8 NT states) = x^T M over K k-steps; with few n-tiles the
@@ -104,7 +128,12 @@ struct WalkMGeom {
   // per warp: 2 stages x 3 operands x K x 32 doubles + 2 x 3 x 32 exponents
   static constexpr int SOPD = SOP ? (6 * K * 32 + 6 * 32 / 2) : 0;
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q + SOP
-  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD) * sizeof(double); }
+  // bulk copies (TMA engine) stage P blocks and operand slots (PIPE only);
+  // two mbarriers, one per buffer parity
+  static constexpr bool TMA = PIPE;
+  static constexpr size_t smem_bytes() {
+    return size_t((NPB + 1) * FRAG + WPC * SOPD + (TMA ? 2 : 0)) * sizeof(double);
+  }
 };
 
 // HESS: Hessian-diagonal variant (a template parameter so the gradient-only
@@ -123,6 +152,33 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
   double* sop_base = smd + size_t(Gm::NPB + 1) * FRAG + size_t(threadIdx.x >> 5) * Gm::SOPD;
+  constexpr bool TMA = Gm::TMA;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smd + size_t(Gm::NPB + 1) * FRAG + size_t(Gm::WPC) * Gm::SOPD);
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(mbar, Gm::WPC + 1);  // lane 0 of every warp + thread 0 (P blocks)
+    mbar_init(mbar + 1, Gm::WPC + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned txP = 0, txW = 0, mphase = 0;  // pending transaction bytes; parity bit per buffer
+  // all staging for a buffer is issued: arm its mbarrier with the bytes
+  auto stage_done = [&](int sb) {
+    if constexpr (TMA) {
+      if ((threadIdx.x & 31) == 0) mbar_arrive_tx(mbar + sb, txW);
+      if (threadIdx.x == 0) mbar_arrive_tx(mbar + sb, txP);
+      txP = txW = 0;
+    }
+  };
+  // wait for a buffer's bulk copies (and every thread's cp.async), then the
+  // CTA barrier (cross-thread visibility, and no one still reads the other buffer)
+  auto stage_wait = [&](int sb) {
+    cpa_wait_all();
+    if constexpr (TMA) {
+      mbar_wait(mbar + sb, (mphase >> sb) & 1u);
+      mphase ^= 1u << sb;
+    }
+    __syncthreads();
+  };
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
   const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
@@ -141,9 +197,17 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   __syncwarp();
 
   // stage one (node, category) matrix in B-fragment order (contiguous copy)
-  auto stage_P = [&](double* buf, const double* tab, int node, int l) {
+  auto stage_P = [&](double* buf, const double* tab, int node, int l, int sb) {
     const double* src = tab + ((node - 1) * L + l) * FRAG;
-    for (int i = tid; i < FRAG / 2; i += CT) cpa16(buf + 2 * i, src + 2 * i);
+    if constexpr (TMA) {
+      if (tid == 0) {
+        bulk_g2s(buf, src, FRAG * sizeof(double), mbar + sb);
+        txP += FRAG * sizeof(double);
+      }
+    } else {
+      (void)sb;
+      for (int i = tid; i < FRAG / 2; i += CT) cpa16(buf + 2 * i, src + 2 * i);
+    }
   };
   // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
   // frag[(ki * NT + ni) * 32 + lane]; with the permuted columns baked into the
@@ -264,6 +328,16 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       return reinterpret_cast<int*>(sop_base + 6 * (K * 32)) + (stage * 3 + which) * 32;
     };
     auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l, const int* xsrc) {
+      if constexpr (TMA) {
+        // the warp's whole slot (K x 32 doubles) and its 8 exponents: two bulk copies
+        if (lane == 0) {
+          bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * (K * 32)), K * 32 * sizeof(double),
+                   mbar + stage);
+          bulk_g2s(xpbuf(stage, which), xsrc - q, 8 * sizeof(int), mbar + stage);
+          txW += K * 32 * sizeof(double) + 8 * sizeof(int);
+        }
+        return;
+      }
       const double2* src = slot_ptr(base, node, l);
       double2* dst = reinterpret_cast<double2*>(opbuf(stage, which)) + lane;
 #pragma unroll
@@ -271,7 +345,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       if constexpr (K & 1)
         cpa8(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane,
              reinterpret_cast<const double*>(src - lane + (K / 2) * 32) + lane);
-      cpa4(xpbuf(stage, which) + lane, xsrc);
+      if (t == 0) cpa4(xpbuf(stage, which) + q, xsrc);
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
       const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
@@ -279,7 +353,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
 #pragma unroll
       for (int ki = 0; ki < K; ++ki)
         cpa8(dst + (ki < 2 * (K / 2) ? ((ki >> 1) * 32 + lane) * 2 + (ki & 1) : (K / 2) * 64 + lane), col + ki * 4);
-      xpbuf(stage, which)[lane] = 0;
+      if (t == 0) xpbuf(stage, which)[q] = 0;
     };
     auto read_op = [&](int stage, int which, double (&v)[K], int& x) {
       const double2* src = reinterpret_cast<const double2*>(opbuf(stage, which)) + lane;
@@ -290,7 +364,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         v[2 * kp + 1] = d.y;
       }
       if constexpr (K & 1) v[K - 1] = reinterpret_cast<const double*>(src - lane + (K / 2) * 32)[lane];
-      x = xpbuf(stage, which)[lane];
+      x = xpbuf(stage, which)[q];
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
       const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
@@ -338,25 +412,28 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (st.z <= N) stage_gather_op(stage, 1, st.z, c1, l);
         else stage_slot_op(stage, 1, E, st.z, l, Ex + exp_idx(st.z, l));
       };
-      if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0);
+      if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0, 0);
       if (sop) stage_post_ops(stc, cc0, cc1, 0, 0);
+      if (PIPE) stage_done(0);
       cpa_commit();
       Mix mix{{}, INT_MIN};
       int i = 0, l = 0;
       for (int u = 0; u < U; ++u) {
         const int par = PIPE ? (u & 1) : 0;
-        cpa_wait_all();
-        __syncthreads();
+        stage_wait(par);
         int l2 = l + 1;
         const bool step_end = l2 == L;
         if (step_end) l2 = 0;
         const bool has_next = u + 1 < U;
         const int4 st2 = step_end ? stn : stc;
         if (PIPE) {
-          if (has_next && st2.x != root) stage_P(pbuf(0, (u + 1) & 1), PM.fpp, st2.x, l2);
-          if (sop && has_next) stage_post_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
+          if (has_next) {
+            if (st2.x != root) stage_P(pbuf(0, (u + 1) & 1), PM.fpp, st2.x, l2, (u + 1) & 1);
+            if (sop) stage_post_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
+            stage_done((u + 1) & 1);
+          }
         } else if (stc.x != root) {
-          stage_P(pbuf(0, 0), PM.fpp, stc.x, l);
+          stage_P(pbuf(0, 0), PM.fpp, stc.x, l, 0);
         }
         cpa_commit();
         double a[K], b[K];
@@ -443,8 +520,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         } else gather(st.z, c1, l, eb);
       };
       auto stage_pre = [&](const int4 st, int l, int par) {
-        if (st.y > N) stage_P(pbuf(0, par), PM.fpt, st.y, l);
-        if (st.z > N) stage_P(pbuf(1, par), PM.fpt, st.z, l);
+        if (st.y > N) stage_P(pbuf(0, par), PM.fpt, st.y, l, par);
+        if (st.z > N) stage_P(pbuf(1, par), PM.fpt, st.z, l, par);
       };
       int4 stc = p.pre[0];
       int4 stn = n > 1 ? p.pre[1] : stc;
@@ -463,6 +540,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       };
       if (PIPE) stage_pre(stc, 0, 0);
       if (sop) stage_pre_ops(stc, cc0, cc1, 0, 0);
+      if (PIPE) stage_done(0);
       cpa_commit();
       // mixtures: [0] den, [1] num_a, [2] num_b, [3] num2_a, [4] num2_b
       Mix mix{{}, INT_MIN};
@@ -471,16 +549,18 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         const int par = PIPE ? (u & 1) : 0;
         const int ca = stc.y, cb = stc.z;
         const bool a_int = ca > N, b_int = cb > N;
-        cpa_wait_all();
-        __syncthreads();
+        stage_wait(par);
         int l2 = l + 1;
         const bool step_end = l2 == L;
         if (step_end) l2 = 0;
         const bool has_next = u + 1 < U;
         const int4 st2 = step_end ? stn : stc;
         if (PIPE) {
-          if (has_next) stage_pre(st2, l2, (u + 1) & 1);
-          if (sop && has_next) stage_pre_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
+          if (has_next) {
+            stage_pre(st2, l2, (u + 1) & 1);
+            if (sop) stage_pre_ops(st2, step_end ? cn0 : cc0, step_end ? cn1 : cc1, l2, (u + 1) & 1);
+            stage_done((u + 1) & 1);
+          }
         } else {
           stage_pre(stc, l, 0);
         }
