@@ -130,7 +130,7 @@ struct WalkMGeom {
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q + SOP
   // bulk copies (TMA engine) stage P blocks and operand slots (PIPE only);
   // two mbarriers, one per buffer parity
-  static constexpr bool TMA = PIPE;
+  static constexpr bool TMA = true;
   static constexpr size_t smem_bytes() {
     return size_t((NPB + 1) * FRAG + WPC * SOPD + (TMA ? 2 : 0)) * sizeof(double);
   }
@@ -173,11 +173,17 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // CTA barrier (cross-thread visibility, and no one still reads the other buffer)
   auto stage_wait = [&](int sb) {
     cpa_wait_all();
-    if constexpr (TMA) {
+    if constexpr (TMA && Gm::PIPE) {
       mbar_wait(mbar + sb, (mphase >> sb) & 1u);
       mphase ^= 1u << sb;
     }
     __syncthreads();
+  };
+  // unbuffered (large MP): the current unit's blocks are staged after the
+  // unit-top barrier and awaited here, right before their first use
+  auto unit_blocks_wait = [&]() {
+    mbar_wait(mbar, mphase & 1u);
+    mphase ^= 1u;
   };
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
@@ -434,6 +440,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           }
         } else if (stc.x != root) {
           stage_P(pbuf(0, 0), PM.fpp, stc.x, l, 0);
+          stage_done(0);  // awaited below (non-root units only)
         }
         cpa_commit();
         double a[K], b[K];
@@ -471,10 +478,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
             if (lane == 0) atomicAdd(Acc, v);
           }
         } else {
-          if (!PIPE) {
-            cpa_wait_all();
-            __syncthreads();
-          }
+          if (!PIPE) unit_blocks_wait();
           double e[K];
           matvec_P(pbuf(0, par), a, e);
           store_slot(E, stc.x, l, e);
@@ -563,6 +567,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           }
         } else {
           stage_pre(stc, l, 0);
+          stage_done(0);
         }
         cpa_commit();
         double qv[K], ea[K], eb[K];
@@ -630,10 +635,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         const double scl = pow2(El - mix.ref);
         for (int r = 0; r < NR; ++r) mix.v[r] = fma(term[r], scl, mix.v[r]);
         // outgoing pre-partials of internal children: q_x = P_x^T top
-        if (!PIPE && (a_int || b_int)) {
-          cpa_wait_all();
-          __syncthreads();
-        }
+        if (!PIPE) unit_blocks_wait();
         auto emit_q = [&](int x, double (&qo)[K], int xbase) {
           const int ex = quad_peak_exp(qo);
           scale_by(qo, ex);
