@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // wait for a buffer's bulk copies (and every thread's cp.async), then the
   // CTA barrier (cross-thread visibility, and no one still reads the other buffer)
   auto stage_wait = [&](int sb) {
+    // this thread's earlier scratch stores (generic proxy) must be ordered
+    // before the bulk copies (async proxy) that other threads issue after the
+    // barrier below and that may read them
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
     cpa_wait_all();
     if constexpr (TMA && Gm::PIPE) {
       mbar_wait(mbar + sb, (mphase >> sb) & 1u);
