@@ -46,32 +46,6 @@ __device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-// mbarrier + 1-D bulk copy (TMA engine) helpers
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, unsigned tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(mb)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mb))
-      : "memory");
-}
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
 // D (8 patterns x 8 NT states) = x^T M over K k-steps; with few n-tiles the
 // even/odd k-steps accumulate separately so enough independent DMMAs are in
 // flight to cover the tensor-pipe latency.
@@ -175,7 +149,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // this thread's earlier scratch stores (generic proxy) must be ordered
     // before the bulk copies (async proxy) that other threads issue after the
     // barrier below and that may read them
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    fence_proxy_async_global();
     cpa_wait_all();
     if constexpr (TMA && Gm::PIPE) {
       mbar_wait(mbar + sb, (mphase >> sb) & 1u);
