@@ -10,6 +10,7 @@
 // Errors are rethrown as the reference's exception types with its messages.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <map>
@@ -116,6 +117,32 @@ struct SitePatternAlignment {
     out.codes.assign(out.taxa.size(), std::vector<int8_t>(size_t(P)));
     for (size_t r = 0; r < out.taxa.size(); ++r)
       for (int p = 0; p < P; ++p) out.codes[r][size_t(p)] = int8_t(pc[r * size_t(P) + size_t(p)]);
+    return out;
+  }
+
+  // The same compression on GPU `device` (pg_compress_codes_gpu), for
+  // alignments too large for the host path; bit-identical result.  codes is
+  // row-major [taxa][sites] int8 (-1 missing).
+  static SitePatternAlignment from_codes_gpu(std::vector<std::string> taxa, const std::vector<int8_t>& codes,
+                                             int64_t sites, int state_count, int device = 0) {
+    if (taxa.empty()) throw std::invalid_argument("alignment: no records");
+    if (int64_t(codes.size()) != int64_t(taxa.size()) * sites)
+      throw std::invalid_argument("alignment: taxa/codes mismatch");
+    void* h = nullptr;
+    int P = 0;
+    check(pg_compress_codes_gpu(int(taxa.size()), sites, codes.data(), 0, state_count, device, &h, &P));
+    std::vector<int8_t> pc(taxa.size() * size_t(P));
+    SitePatternAlignment out;
+    out.weights.resize(size_t(P));
+    const int rc = pg_compress_result_gpu(h, pc.data(), out.weights.data(), nullptr, nullptr);
+    pg_compress_free_gpu(h);
+    check(rc);
+    out.state_count = state_count;
+    out.taxa = std::move(taxa);
+    out.codes.assign(out.taxa.size(), std::vector<int8_t>(size_t(P)));
+    for (size_t r = 0; r < out.taxa.size(); ++r)
+      std::copy(pc.begin() + std::ptrdiff_t(r * size_t(P)), pc.begin() + std::ptrdiff_t((r + 1) * size_t(P)),
+                out.codes[r].begin());
     return out;
   }
 };

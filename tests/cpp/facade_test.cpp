@@ -21,6 +21,16 @@ int main() {
   for (int i = 0; i < 4; ++i) jc.q[size_t(i * 4 + i)] = -1.0;
   jc.pi.assign(4, 0.25);
   auto aln = SitePatternAlignment::from_codes({"A", "B"}, {{0}, {1}}, 4);
+  {
+    // GPU compression through the facade: bit-identical to the host path
+    const std::vector<std::vector<int>> cols = {{0, 1, 0, 2, -1, 1, 0}, {3, 3, 3, 1, 2, 3, 3}};
+    std::vector<int8_t> flat;
+    for (const auto& row : cols)
+      for (int c : row) flat.push_back(int8_t(c));
+    auto host = SitePatternAlignment::from_codes({"x", "y"}, cols, 4);
+    auto dev = SitePatternAlignment::from_codes_gpu({"x", "y"}, flat, 7, 4);
+    expect(host.weights == dev.weights && host.codes == dev.codes, "GPU compression matches the host");
+  }
   LikelihoodEngine engine(tree, aln, jc, RateCategories::single());
   const double same = 0.25 + 0.75 * std::exp(-4.0 * 0.3 / 3.0);
   const double site = 0.25 * (1.0 - same) / 3.0;
