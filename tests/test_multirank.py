@@ -105,3 +105,37 @@ def test_shard_ranges_partition():
             assert blocks[0][0] == 0 and blocks[-1][1] == P
             for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
                 assert a1 == b0 and a0 <= a1
+
+
+@pytest.mark.gpu
+def test_single_rank_nccl_device_path():
+    """The NCCL device path of ShardedEngine (pg_evaluate_device into a CUDA
+    buffer + all-reduce on the engine's stream) against the oracle, with a
+    one-rank NCCL group (a multi-rank NCCL group needs one GPU per rank)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_12146_b200 import synth
+    from paper_1905_12146_b200.api import RateCategories, SitePatternAlignment, SubstitutionModel, Tree
+    from paper_1905_12146_b200.sharding import ShardedEngine
+    from tests.helpers import assert_logl, assert_vec, oracle_for
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        inst = synth.generate("C4", seed=9, sites=400, tips=60)
+        labels = inst.labels()
+        tree = Tree(inst.tip_count, inst.parent, inst.children,
+                    np.concatenate([[0.0], inst.branch_lengths, [0.0]]), labels, inst.post_order)
+        aln = SitePatternAlignment(labels[1:inst.tip_count + 1], inst.states, inst.codes, inst.weights)
+        sh = ShardedEngine(tree, aln, SubstitutionModel(inst.q, inst.pi, inst.reversible),
+                           RateCategories(inst.cat_rates, inst.cat_probs))
+        assert sh._device_path
+        rep = sh.branch_gradient(True)
+        ll, g, h = oracle_for(inst, blocks=4).branch_gradient(True)
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    finally:
+        dist.destroy_process_group()
