@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--sites", type=int, default=None, help="override column count (testing only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=None, help="patterns in the CPU baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work timed for the cpu_baseline (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period in the timed region (0: off)")
     return ap.parse_args()
@@ -160,23 +161,53 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
-def cpu_baseline(inst, sample, threads):
-    """Oracle (CPU restatement of engine.hpp) on a bounded pattern sample:
-    invalidate + branch_gradient, median of 3 after a warm-up
-    (validation.hpp:281-286 idiom)."""
+def cpu_baseline(inst, sample, threads, target_s=10.0):
+    """Oracle (CPU restatement of engine.hpp) timed with the reference's
+    `invalidate_caches(); branch_gradient()` idiom (validation.hpp:281-286).
+    One evaluation costs a + b P: a fixed part (the B x L transition
+    matrices) and a part linear in the pattern count.  The oracle keeps full
+    per-node partial grids, so a sample is capped in memory (`sample`
+    patterns); two sample sizes (S and S/4) are timed repeatedly until about
+    target_s seconds of CPU work, and the full-workload time is a + b P
+    (time full-tree chunks, extrapolate linearly in P).
+    Returns (pattern-branch/s, description)."""
     from tests.helpers import oracle_for
 
-    sub = inst.slice_patterns(0, min(sample, inst.patterns))
-    ref = oracle_for(sub, blocks=threads)
-    ref.branch_gradient()
-    times = []
-    for _ in range(3):
+    P = inst.patterns
+    S = min(sample, P)
+    big = oracle_for(inst.slice_patterns(0, S), blocks=threads)
+    small = None if S == P else oracle_for(inst.slice_patterns(0, max(1, S // 4)), blocks=threads)
+    s1 = max(1, S // 4)
+
+    def timed(ref):
         ref.invalidate_caches()
         t0 = time.perf_counter()
         ref.branch_gradient()
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return sub.patterns, t
+        return time.perf_counter() - t0
+
+    timed(big)  # warm-up
+    if small is not None:
+        timed(small)
+    tb, ts, total = [], [], 0.0
+    while len(tb) < 3 or total < target_s:
+        tb.append(timed(big))
+        total += tb[-1]
+        if small is not None:
+            ts.append(timed(small))
+            total += ts[-1]
+        if len(tb) >= 50:
+            break
+    t_big = statistics.median(tb)
+    if small is None:
+        t_full, how = t_big, f"all {P} patterns, median of {len(tb)}"
+    else:
+        t_small = statistics.median(ts)
+        slope = max(0.0, (t_big - t_small) / (S - s1))
+        fixed = max(0.0, t_big - slope * S)
+        t_full = fixed + slope * P
+        how = (f"samples of {S} and {s1} of {P} patterns (median of {len(tb)} each), fitted "
+               f"{fixed * 1e3:.1f} ms + {slope * 1e6:.3f} us/pattern, extrapolated to {P}")
+    return P * inst.branches / t_full, f"{how}; {total:.1f} s of CPU time"
 
 
 def cpu_model():
@@ -215,7 +246,26 @@ def run_reference(args, inst):
         ref.invalidate_caches()
         ref.branch_gradient()
     t = (time.perf_counter() - t0) / args.steps
+    # one evaluation is a + b P (fixed transition-matrix build + per pattern):
+    # the fixed part is measured on a quarter sample and the step time is
+    # extrapolated to the full pattern count, so the sample
+    # does not charge the fixed part to too few patterns
+    how = f"{sub.patterns} of {inst.patterns} patterns per step"
     value = sub.patterns * B / t
+    if sub.patterns < inst.patterns and sub.patterns >= 8:
+        small = oracle_for(inst.slice_patterns(0, sub.patterns // 4), blocks=threads)
+        ts = []
+        for _ in range(3):
+            small.invalidate_caches()
+            t1 = time.perf_counter()
+            small.branch_gradient()
+            ts.append(time.perf_counter() - t1)
+        t_small = statistics.median(ts)
+        slope = max(0.0, (t - t_small) / (sub.patterns - sub.patterns // 4))
+        fixed = max(0.0, t - slope * sub.patterns)
+        value = inst.patterns * B / (fixed + slope * inst.patterns)
+        how += (f", extrapolated to all {inst.patterns} ({fixed * 1e3:.1f} ms fixed + "
+                f"{slope * 1e6:.3f} us/pattern, fixed part from a {sub.patterns // 4}-pattern sample)")
     line = {
         "impl": "reference", "metric": "pattern x branch gradient updates/s (full logL + grad eval)",
         "value": value, "unit": "pattern-branch/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
@@ -225,8 +275,7 @@ def run_reference(args, inst):
                    "branches": B, "tips": inst.tip_count, "states": inst.states,
                    "categories": len(inst.cat_rates)},
         "cpu_baseline": {"value": value, "unit": "pattern-branch/s", "cores": threads, "kind": "port",
-                         "sample": f"{sub.patterns} of {inst.patterns} patterns, full tree, {threads} pattern blocks "
-                                   f"on std::threads; {cpu_model()}"},
+                         "sample": f"{how}, full tree, {threads} pattern blocks on std::threads; {cpu_model()}"},
         "e2e": {"value": value, "unit": "pattern-branch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -396,11 +445,9 @@ def main():
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
             sample = args.cpu_sample or default_sample(inst)
-            n, tcpu = cpu_baseline(inst, sample, threads)
-            line["cpu_baseline"] = {"value": n * B / tcpu, "unit": "pattern-branch/s", "cores": threads,
-                                    "kind": "port",
-                                    "sample": f"{n} of {P_total} patterns, full tree, one invalidate+gradient "
-                                              f"(median of 3); {cpu_model()}"}
+            cpu_value, how = cpu_baseline(inst, sample, threads, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": cpu_value, "unit": "pattern-branch/s", "cores": threads, "kind": "port",
+                                    "sample": f"full tree, invalidate+gradient: {how}; {cpu_model()}"}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

@@ -155,7 +155,10 @@ class Rng:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_rng_free(self.h)
+            try:
+                lib().orc_rng_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
 
     def next(self) -> int:
         return int(lib().orc_rng_next(self.h))
@@ -188,7 +191,10 @@ class Tree:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_tree_free(self.h)
+            try:
+                lib().orc_tree_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def node_count(self):
@@ -327,7 +333,10 @@ class Model:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_model_free(self.h)
+            try:
+                lib().orc_model_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @staticmethod
     def gtr(exch, freqs):
@@ -375,7 +384,10 @@ class Alignment:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_aln_free(self.h)
+            try:
+                lib().orc_aln_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @staticmethod
     def from_codes(codes, m, labels=None) -> "Alignment":
@@ -457,7 +469,10 @@ class Engine:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_engine_free(self.h)
+            try:
+                lib().orc_engine_free(self.h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def branch_lengths(self):

@@ -521,7 +521,10 @@ class LikelihoodEngine:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().pg_destroy(h)
+            try:
+                lib().pg_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     # --- accessors (engine.hpp:112-114)
