@@ -201,3 +201,32 @@ def test_deep_caterpillar_rescaling(m, L, tips, sites):
     off, _ = _caterpillar_pair(m, L, tips, sites, 31 + m, 0.3, disable_rescaling=True)
     with pytest.raises(pg.RuntimeFailure, match="underflow"):
         off.log_likelihood()
+
+
+@pytest.mark.parametrize("m", [4, 20, 61])
+def test_extreme_branch_lengths(m):
+    """Zero-length branches (P = I exactly, substitution.hpp:151: indicator
+    tip vectors, zero lanes) and very long ones (P -> stationary rows) through
+    every kernel family."""
+    rng = np.random.default_rng(5 + m)
+    q, pi = _reversible(m, rng)
+    mo = O.Model(q, pi, True)
+    r = O.Rng(40 + m)
+    tree_o = O.Tree.random(r, 12, 0.02, 0.5)
+    bl = tree_o.branch_lengths.copy()
+    bl[::4] = 0.0
+    bl[1::5] = 40.0
+    rates, probs = O.discrete_gamma(0.5, 4)
+    codes = O.simulate_states(tree_o, mo, rates, probs, bl, 120, 9 + m)  # data consistent with P = I
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    tree_x = O.Tree.from_arrays(tree_o.tip_count, tree_o.parent, tree_o.children, bl, tree_o.post_order)
+    ref = O.Engine(tree_x, O.Alignment.from_codes(codes, m, labels), mo, rates, probs)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children, np.concatenate([[0.0], bl, [0.0]]),
+                tree_o.labels, tree_o.post_order)
+    eng = LikelihoodEngine(tree, SitePatternAlignment.from_codes(labels, codes, m), SubstitutionModel(q, pi, True),
+                           RateCategories(np.asarray(rates), np.asarray(probs)), EngineOptions())
+    ll, g, h = ref.branch_gradient(True)
+    rep = eng.branch_gradient(True)
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
