@@ -30,25 +30,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cpa_commit_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
-}
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-// D (8 patterns x 8 NT states) = x^T M over K k-steps; with few n-tiles the
-// even/odd k-steps accumulate separately so enough independent DMMAs are in
-// flight to cover the tensor-pipe latency.
+// D (8 patterns x 8 NT states) = x^T M over K k-steps, one accumulator chain
+// per n-tile (NT independent chains in flight; the other resident warps cover
+// the 26-cycle dependent-DMMA latency, profiles/dmma_latency_b200.jsonl).
 template <int K, int NT, class F>
 __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT][2], F bfrag) {
   // one accumulator chain per n-tile: at the 128-register cap the even/odd
@@ -101,13 +90,9 @@ struct WalkMGeom {
   static constexpr int WPC = MP <= 32 ? PG_WALKM_WPC_SMALL : 4;
   // per warp: 2 stages x 3 operands x K x 32 doubles + 2 x 3 x 32 exponents
   static constexpr int SOPD = SOP ? (6 * K * 32 + 6 * 32 / 2) : 0;
-  // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q + SOP
-  // bulk copies (TMA engine) stage P blocks and operand slots (PIPE only);
-  // two mbarriers, one per buffer parity
-  static constexpr bool TMA = true;
-  static constexpr size_t smem_bytes() {
-    return size_t((NPB + 1) * FRAG + WPC * SOPD + (TMA ? 2 : 0)) * sizeof(double);
-  }
+  // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
+  // + SOP + two mbarriers (one per buffer parity) for the bulk copies
+  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD + 2) * sizeof(double); }
 };
 
 // HESS: Hessian-diagonal variant (a template parameter so the gradient-only
@@ -126,9 +111,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
   double* sop_base = smd + size_t(Gm::NPB + 1) * FRAG + size_t(threadIdx.x >> 5) * Gm::SOPD;
-  constexpr bool TMA = Gm::TMA;
+  // P blocks and operand slots are staged with 1-D bulk copies (TMA engine)
+  // that complete on these mbarriers
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smd + size_t(Gm::NPB + 1) * FRAG + size_t(Gm::WPC) * Gm::SOPD);
-  if (TMA && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     mbar_init(mbar, Gm::WPC + 1);  // lane 0 of every warp + thread 0 (P blocks)
     mbar_init(mbar + 1, Gm::WPC + 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -137,11 +123,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   unsigned txP = 0, txW = 0, mphase = 0;  // pending transaction bytes; parity bit per buffer
   // all staging for a buffer is issued: arm its mbarrier with the bytes
   auto stage_done = [&](int sb) {
-    if constexpr (TMA) {
-      if ((threadIdx.x & 31) == 0) mbar_arrive_tx(mbar + sb, txW);
-      if (threadIdx.x == 0) mbar_arrive_tx(mbar + sb, txP);
-      txP = txW = 0;
-    }
+    if ((threadIdx.x & 31) == 0) mbar_arrive_tx(mbar + sb, txW);
+    if (threadIdx.x == 0) mbar_arrive_tx(mbar + sb, txP);
+    txP = txW = 0;
   };
   // wait for a buffer's bulk copies (and every thread's cp.async), then the
   // CTA barrier (cross-thread visibility, and no one still reads the other buffer)
@@ -151,7 +135,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // barrier below and that may read them
     fence_proxy_async_global();
     cpa_wait_all();
-    if constexpr (TMA && Gm::PIPE) {
+    if constexpr (Gm::PIPE) {
       mbar_wait(mbar + sb, (mphase >> sb) & 1u);
       mphase ^= 1u << sb;
     }
@@ -182,15 +166,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
 
   // stage one (node, category) matrix in B-fragment order (contiguous copy)
   auto stage_P = [&](double* buf, const double* tab, int node, int l, int sb) {
-    const double* src = tab + ((node - 1) * L + l) * FRAG;
-    if constexpr (TMA) {
-      if (tid == 0) {
-        bulk_g2s(buf, src, FRAG * sizeof(double), mbar + sb);
-        txP += FRAG * sizeof(double);
-      }
-    } else {
-      (void)sb;
-      for (int i = tid; i < FRAG / 2; i += CT) cpa16(buf + 2 * i, src + 2 * i);
+    if (tid == 0) {
+      bulk_g2s(buf, tab + ((node - 1) * L + l) * FRAG, FRAG * sizeof(double), mbar + sb);
+      txP += FRAG * sizeof(double);
     }
   };
   // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
@@ -306,30 +284,20 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       if constexpr (K & 1) __stcg(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane, v[K - 1]);
     };
     // ---- staged operands (SOP): the next unit's operands are copied into a
-    // per-warp shared stage with cp.async while this unit computes
+    // per-warp shared stage (bulk copies for scratch slots, per-lane cp.async
+    // gathers for tip columns) while this unit computes
     auto opbuf = [&](int stage, int which) -> double* { return sop_base + (stage * 3 + which) * (K * 32); };
     auto xpbuf = [&](int stage, int which) -> int* {
       return reinterpret_cast<int*>(sop_base + 6 * (K * 32)) + (stage * 3 + which) * 32;
     };
+    // the warp's whole slot (K x 32 doubles) and its 8 exponents: two bulk copies
     auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l, const int* xsrc) {
-      if constexpr (TMA) {
-        // the warp's whole slot (K x 32 doubles) and its 8 exponents: two bulk copies
-        if (lane == 0) {
-          bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * (K * 32)), K * 32 * sizeof(double),
-                   mbar + stage);
-          bulk_g2s(xpbuf(stage, which), xsrc - q, 8 * sizeof(int), mbar + stage);
-          txW += K * 32 * sizeof(double) + 8 * sizeof(int);
-        }
-        return;
+      if (lane == 0) {
+        bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * (K * 32)), K * 32 * sizeof(double),
+                 mbar + stage);
+        bulk_g2s(xpbuf(stage, which), xsrc - q, 8 * sizeof(int), mbar + stage);
+        txW += K * 32 * sizeof(double) + 8 * sizeof(int);
       }
-      const double2* src = slot_ptr(base, node, l);
-      double2* dst = reinterpret_cast<double2*>(opbuf(stage, which)) + lane;
-#pragma unroll
-      for (int kp = 0; kp < K / 2; ++kp) cpa16(dst + kp * 32, src + kp * 32);
-      if constexpr (K & 1)
-        cpa8(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane,
-             reinterpret_cast<const double*>(src - lane + (K / 2) * 32) + lane);
-      if (t == 0) cpa4(xpbuf(stage, which) + q, xsrc);
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
       const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
