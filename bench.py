@@ -301,8 +301,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_gen = time.perf_counter()
-    threads = max(1, (os.cpu_count() or 1) // max(world, 1))
-    inst = synth.generate(args.config, seed=SEED, sites=args.sites, threads=threads)
+    inst = synth.generate_shared(args.config, rank, world, (lambda: torch.distributed.barrier()) if world > 1 else None,
+                                 tag=str(os.getppid()), seed=SEED, sites=args.sites)
     t_gen = time.perf_counter() - t_gen
     P_total = inst.patterns
     p0, p1 = P_total * rank // world, P_total * (rank + 1) // world

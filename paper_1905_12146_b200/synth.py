@@ -70,6 +70,19 @@ class Instance:
     def labels(self):
         return [""] + [f"t{i}" for i in range(1, self.tip_count + 1)] + [""] * (self.tip_count - 1)
 
+    def save(self, path):
+        """Uncompressed .npz (fast to share between the ranks of one node)."""
+        import dataclasses
+        np.savez(path, **{k: np.asarray(v) for k, v in dataclasses.asdict(self).items()})
+
+    @staticmethod
+    def load(path) -> "Instance":
+        z = np.load(path, allow_pickle=False)
+        return Instance(str(z["name"]), int(z["tip_count"]), z["parent"], z["children"], z["post_order"],
+                        z["branch_lengths"], z["durations"], z["branch_rates"], z["q"], z["pi"],
+                        bool(z["reversible"]), z["cat_rates"], z["cat_probs"], z["codes"], z["weights"],
+                        bool(z["clock"]))
+
     def slice_patterns(self, p0, p1) -> "Instance":
         import dataclasses
         return dataclasses.replace(self, codes=np.ascontiguousarray(self.codes[:, p0:p1]),
@@ -124,6 +137,28 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
         L.pg_synth_free(h)
     return Instance(name, N, parent, children.reshape(n + 1, 2), post, blen, dt, rr, q.reshape(mm, mm), pi,
                     bool(rev.value), cr, cp, codes, w, bool(spec.clock))
+
+
+def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: int = 12146,
+                    sites: int | None = None) -> Instance:
+    """One rank of a node simulates the workload with every host core and
+    shares it through node-local shared memory; the other ranks load it
+    (identical input everywhere; each rank then keeps its pattern shard).
+    `barrier` is a callable synchronising all ranks (e.g. dist.barrier)."""
+    import os
+
+    if world <= 1:
+        return generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1)
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    path = os.path.join(shm, f"pg_synth_{name}_{seed}_{sites or 0}_{tag}.npz")
+    if rank == 0:
+        generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1).save(path)
+    barrier()
+    inst = Instance.load(path)
+    barrier()
+    if rank == 0:
+        os.remove(path)
+    return inst
 
 
 def engine_for(inst: Instance, options=None):

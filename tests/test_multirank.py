@@ -139,3 +139,39 @@ def test_single_rank_nccl_device_path():
         assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
     finally:
         dist.destroy_process_group()
+
+
+def _share_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_1905_12146_b200 import synth
+
+        inst = synth.generate_shared("C2", rank, world, dist.barrier, tag=f"test{port}", seed=3, sites=700)
+        q.put((rank, inst.patterns, int(inst.codes.astype(np.int64).sum()), int(inst.weights.sum()),
+               float(inst.branch_lengths.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_workload_generation():
+    """bench.py's multi-rank setup: rank 0 simulates, the others load the
+    identical instance from node-local shared memory."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_1905_12146_b200 import synth
+
+    ref = synth.generate("C2", seed=3, sites=700)
+    want = (ref.patterns, int(ref.codes.astype(np.int64).sum()), int(ref.weights.sum()), float(ref.branch_lengths.sum()))
+    for r in res:
+        assert r[1:] == want
