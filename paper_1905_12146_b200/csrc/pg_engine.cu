@@ -789,7 +789,7 @@ void pg_engine::launch_tc() {
   if (smem > 48 * 1024)
     PG_CUDA(cudaFuncSetAttribute(pgk::tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid{unsigned(B()), unsigned(L), 1u};
-  pgk::tc_kernel<<<grid, 128, smem, stream>>>(p);
+  pgk::tc_kernel<<<grid, m > 24 ? 512 : 128, smem, stream>>>(p);  // codon blocks: one per SM (smem), more threads
   PG_CUDA(cudaGetLastError());
 }
 

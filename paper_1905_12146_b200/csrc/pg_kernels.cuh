@@ -207,10 +207,14 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
     for (int e = threadIdx.x; e < mm; e += blockDim.x) P[e] = (e / m == e % m) ? 1.0 : 0.0;
     __syncthreads();
   } else if (p.have_eigen && qi == 0) {
+    // P = U diag(e^{w t}) U^-1: the m exponentials once, then the contraction
+    double* ew = sm + mm;
+    for (int k = threadIdx.x; k < m; k += blockDim.x) ew[k] = exp(p.eig_w[k] * t);
+    __syncthreads();
     for (int e = threadIdx.x; e < mm; e += blockDim.x) {
       const int i = e / m, j = e % m;
       double s = 0.0;
-      for (int k = 0; k < m; ++k) s = fma(p.eig_u[i * m + k] * exp(p.eig_w[k] * t), p.eig_ui[k * m + j], s);
+      for (int k = 0; k < m; ++k) s = fma(__ldg(p.eig_u + i * m + k) * ew[k], __ldg(p.eig_ui + k * m + j), s);
       P[e] = s;
     }
     __syncthreads();
