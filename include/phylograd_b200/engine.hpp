@@ -11,6 +11,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdint>
 #include <map>
@@ -179,6 +180,7 @@ struct EngineOptions {
   bool force_rescaling = false;
   bool disable_rescaling = false;
   int device = 0;
+  bool capture_partials = false;  // keep per-node partials for the engine.hpp:134-141 accessors (debug)
 };
 
 // engine.hpp:39-45
@@ -213,6 +215,7 @@ class LikelihoodEngine {
     o.force_rescaling = options.force_rescaling;
     o.disable_rescaling = options.disable_rescaling;
     o.device = options.device;
+    o.capture_partials = options.capture_partials ? 1 : 0;
     check(pg_create(&o, &h_));
     std::vector<int32_t> ch(size_t(2 * (tree.node_count() + 1)));
     for (int i = 0; i <= tree.node_count(); ++i) {
@@ -229,6 +232,9 @@ class LikelihoodEngine {
     std::vector<double> b(tree.branch_length.begin() + 1, tree.branch_length.begin() + tree.node_count());
     set_branch_lengths(b);
     patterns_ = alignment.pattern_count();
+    states_ = m;
+    tip_codes_ = std::move(codes);
+    ambiguity_ = alignment.ambiguity;
   }
   ~LikelihoodEngine() { pg_destroy(h_); }
   LikelihoodEngine(const LikelihoodEngine&) = delete;
@@ -265,7 +271,65 @@ class LikelihoodEngine {
   }
   pg_engine* handle() { return h_; }
 
+  // engine.hpp:134-141 (needs EngineOptions::capture_partials): partials as
+  // column-major m x P (entry (s, p) at p * m + s), log scalers per pattern.
+  // Tips: their 0/1 (or ambiguity) partials and zero scalers, like the reference.
+  std::vector<double> post_partial(int node, int category) {
+    if (node >= 1 && node <= tree_.tip_count) return tip_partial(node);
+    return partials(node, category).post;
+  }
+  std::vector<double> pre_partial(int node, int category) { return partials(node, category).pre; }
+  std::vector<double> post_scaler(int node) {
+    if (node >= 1 && node <= tree_.tip_count) return std::vector<double>(size_t(patterns_), 0.0);
+    return partials(node, 0).post_scaler;
+  }
+  std::vector<double> pre_scaler(int node) { return partials(node, 0).pre_scaler; }
+  // engine.hpp:168-180: logL from the partials meeting at `node` (Eq. 8)
+  double log_likelihood_at_node(int node, const std::vector<int64_t>& weights) {
+    branch_gradient();
+    const int m = states_, P = patterns_;
+    std::vector<double> mix(size_t(P), 0.0);
+    for (int l = 0; l < categories_.count(); ++l) {
+      const auto a = post_partial(node, l), b = pre_partial(node, l);
+      for (int p = 0; p < P; ++p) {
+        double d = 0.0;
+        for (int i = 0; i < m; ++i) d += a[size_t(p) * m + i] * b[size_t(p) * m + i];
+        mix[size_t(p)] += categories_.probs[size_t(l)] * d;
+      }
+    }
+    const auto sa = post_scaler(node), sb = pre_scaler(node);
+    double ll = 0.0;
+    for (int p = 0; p < P; ++p)
+      ll += double(weights[size_t(p)]) * (std::log(mix[size_t(p)]) + sa[size_t(p)] + sb[size_t(p)]);
+    return ll;
+  }
+
  private:
+  struct NodePartials {
+    std::vector<double> post, pre, post_scaler, pre_scaler;
+  };
+  NodePartials partials(int node, int category) {
+    NodePartials r;
+    const size_t mp = size_t(states_) * size_t(patterns_);
+    r.post.resize(mp);
+    r.pre.resize(mp);
+    r.post_scaler.resize(size_t(patterns_));
+    r.pre_scaler.resize(size_t(patterns_));
+    check(pg_get_partials(h_, node, category, r.post.data(), r.pre.data(), r.post_scaler.data(),
+                          r.pre_scaler.data()));
+    return r;
+  }
+  std::vector<double> tip_partial(int tip) const {
+    const int m = states_, P = patterns_;
+    std::vector<double> v(size_t(m) * size_t(P), 0.0);
+    for (int p = 0; p < P; ++p) {
+      const int c = tip_codes_[size_t(tip - 1) * size_t(P) + size_t(p)];
+      for (int i = 0; i < m; ++i)
+        v[size_t(p) * m + i] = c < 0 ? 1.0 : c < m ? (i == c ? 1.0 : 0.0) : ambiguity_[size_t(c - m) * m + i];
+    }
+    return v;
+  }
+
   GradientReport eval(int flags) {
     GradientReport r;
     r.branch_gradient.assign(size_t(tree_.branch_count()), 0.0);
@@ -281,7 +345,9 @@ class LikelihoodEngine {
   Tree tree_;
   RateCategories categories_;
   pg_engine* h_ = nullptr;
-  int patterns_ = 0;
+  int patterns_ = 0, states_ = 0;
+  std::vector<int8_t> tip_codes_;  // [tip][pattern] (for the tip partial accessors)
+  std::vector<double> ambiguity_;  // [class][m]
 };
 
 }  // namespace phylograd_b200

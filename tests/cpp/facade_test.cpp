@@ -59,6 +59,23 @@ int main() {
     threw = std::string(e.what()).find("not found") != std::string::npos;
   }
   expect(threw, "unbound tip -> 'not found'");
+  {
+    // engine.hpp:134-141 accessors + Eq. 8 node invariance (test_engine.cpp:133-147)
+    Tree t5 = parse_newick("((A:0.1,B:0.2):0.05,(C:0.3,(D:0.1,E:0.15):0.2):0.1);");
+    auto a5 = SitePatternAlignment::from_codes({"A", "B", "C", "D", "E"},
+                                               {{0, 1, 2, 3, -1, 0}, {0, 1, 2, 2, 1, 0}, {1, 1, 2, 3, 0, 3},
+                                                {0, 3, 2, 3, 1, 0}, {0, 1, 0, 3, 1, 2}},
+                                               4);
+    EngineOptions opts;
+    opts.capture_partials = true;
+    LikelihoodEngine e5(t5, a5, jc, discrete_gamma_categories(0.7, 3), opts);
+    const double ll = e5.log_likelihood();
+    bool ok = true;
+    for (int k = 1; k <= t5.node_count(); ++k)
+      ok = ok && std::fabs(e5.log_likelihood_at_node(k, a5.weights) - ll) < 1e-11 * std::fabs(ll);
+    expect(ok, "log_likelihood_at_node equals logL at every node");
+    expect(e5.post_partial(1, 0).size() == size_t(4 * a5.pattern_count()), "post_partial is m x P");
+  }
   auto cats = discrete_gamma_categories(0.5, 4);
   expect(cats.count() == 4 && std::fabs(cats.rates[0] - 0.0290777) < 1e-6, "discrete gamma(0.5, 4)");
   return failures == 0 ? 0 : 1;
