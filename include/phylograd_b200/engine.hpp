@@ -235,6 +235,7 @@ class LikelihoodEngine {
     states_ = m;
     tip_codes_ = std::move(codes);
     ambiguity_ = alignment.ambiguity;
+    weights_ = alignment.weights;
   }
   ~LikelihoodEngine() { pg_destroy(h_); }
   LikelihoodEngine(const LikelihoodEngine&) = delete;
@@ -285,7 +286,8 @@ class LikelihoodEngine {
   }
   std::vector<double> pre_scaler(int node) { return partials(node, 0).pre_scaler; }
   // engine.hpp:168-180: logL from the partials meeting at `node` (Eq. 8)
-  double log_likelihood_at_node(int node, const std::vector<int64_t>& weights) {
+  double log_likelihood_at_node(int node) {
+    const std::vector<int64_t>& weights = weights_;
     branch_gradient();
     const int m = states_, P = patterns_;
     std::vector<double> mix(size_t(P), 0.0);
@@ -348,6 +350,7 @@ class LikelihoodEngine {
   int patterns_ = 0, states_ = 0;
   std::vector<int8_t> tip_codes_;  // [tip][pattern] (for the tip partial accessors)
   std::vector<double> ambiguity_;  // [class][m]
+  std::vector<int64_t> weights_;   // pattern multiplicities
 };
 
 }  // namespace phylograd_b200

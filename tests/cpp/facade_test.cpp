@@ -72,7 +72,7 @@ int main() {
     const double ll = e5.log_likelihood();
     bool ok = true;
     for (int k = 1; k <= t5.node_count(); ++k)
-      ok = ok && std::fabs(e5.log_likelihood_at_node(k, a5.weights) - ll) < 1e-11 * std::fabs(ll);
+      ok = ok && std::fabs(e5.log_likelihood_at_node(k) - ll) < 1e-11 * std::fabs(ll);
     expect(ok, "log_likelihood_at_node equals logL at every node");
     expect(e5.post_partial(1, 0).size() == size_t(4 * a5.pattern_count()), "post_partial is m x P");
   }
