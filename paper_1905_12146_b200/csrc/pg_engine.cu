@@ -22,7 +22,10 @@
 
 void* pg_walk4_kernel_lc4(bool homog, bool hess, int nc);
 void* pg_walk4_kernel_lc2(bool homog, bool hess, int nc);
-static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv) {
+void* pg_walk4_kernel_l12(bool homog, bool hess, int nc, int L);
+// L = 4: lcv 4 (one lane per pattern) or 2 (two lanes); L = 1, 2: one lane
+static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
+  if (L != 4) return pg_walk4_kernel_l12(homog, hess, nc, L);
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
 }
 int pg_walk4_nc(int nc);
@@ -374,6 +377,7 @@ struct pg_engine {
     if (!has_model) throw std::logic_error("engine: set the model before branch generators");
     if (branch < 1 || branch > B()) throw std::invalid_argument("branch generator: branch out of range");
     check_generator(qq, m);
+    if (branch_q.empty()) geometry_dirty = true;  // kernel variant (and its occupancy) changes
     branch_q[branch] = std::vector<double>(qq, qq + m * m);
     model_dirty = tc_dirty = true;
     invalidate();
@@ -530,16 +534,22 @@ struct pg_engine {
     ntiles = (P + TP - 1) / TP;
     // specialised pipelined 4-state kernel (pg_walk4.cuh)
     nc4 = MP == 4 ? pg_walk4_nc(NC) : 0;
-    use_walk4 = MP == 4 && LC == 4 && G == 1 && L == 4 && !opt.capture_partials && nc4 > 0;
+    // pipelined 4-state kernel: 4 categories (one or two lanes per pattern) or
+    // 1 / 2 categories (one lane per pattern)
+    use_walk4 = MP == 4 && G == 1 && LC == L && (L == 4 || L == 2 || L == 1) && !opt.capture_partials && nc4 > 0;
     walk_smem = 0;
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
       // one lane per pattern unless that leaves fewer than ~2 tiles per
       // resident warp slot (measured: C3 153 ms LCV=4 vs 180 ms LCV=2;
       // C2 1.72 ms vs 1.55 ms)
-      walk4_lcv = (int64_t(P) / 32 >= int64_t(num_sms) * 8 * 2) ? 4 : 2;
-      if (const char* v = std::getenv("PG_WALK4_LCV")) walk4_lcv = std::atoi(v) == 4 ? 4 : 2;
-      G = 4 / walk4_lcv;
+      if (L == 4) {
+        walk4_lcv = (int64_t(P) / 32 >= int64_t(num_sms) * 8 * 2) ? 4 : 2;
+        if (const char* v = std::getenv("PG_WALK4_LCV")) walk4_lcv = std::atoi(v) == 4 ? 4 : 2;
+      } else {
+        walk4_lcv = L;  // one lane per pattern holds every category
+      }
+      G = L / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);
       const size_t tcb = size_t(L) * NC * 4;
       walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
@@ -750,9 +760,9 @@ int pg_engine::walk_max_blocks_per_sm() {
     return std::max(nb, 1);
   }
   if (use_walk4) {
-    // occupancy of the heaviest variant (per-branch Q + Hessian) bounds the grid
-    for (int v = 0; v < 4; ++v) {
-      const void* fn = pg_walk4_kernel(v & 1, v & 2, NC, walk4_lcv);
+    // occupancy of the model's variants (with and without the Hessian) bounds the grid
+    for (int v = 0; v < 2; ++v) {
+      const void* fn = pg_walk4_kernel(branch_q.empty(), v & 1, NC, walk4_lcv, L);
       PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
@@ -853,7 +863,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
     }
-    void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv);
+    void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv, L);
     void* args[] = {&p4};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
                              walk_smem, stream));

@@ -58,14 +58,17 @@ __device__ __forceinline__ int peak_exponent(int hmax) {
 // 2^-ex as a double (exact; ex in [-1021, 1022]).
 __device__ __forceinline__ double pow2_neg(int ex) { return __hiloint2double((1023 - ex) << 20, 0); }
 
-// LCV = categories per lane (4: one lane per pattern, 32 patterns per warp
-// tile; 2: two lanes per pattern, 16 patterns per tile, half the registers
-// and shared memory per warp -> more resident warps).
-template <bool HOMOG, bool HESS, int NC, int LCV>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, (LCV == 4 ? 2 : 3))
+// LT = rate categories (4, 2 or 1); LCV = categories per lane (LT: one lane
+// per pattern, 32 patterns per warp tile; LT/2: two lanes per pattern, 16
+// patterns per tile, half the registers and shared memory per warp -> more
+// resident warps).
+template <bool HOMOG, bool HESS, int NC, int LCV, int LT = 4>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32,
+                                  (LCV == 4 || (LCV == 2 && LT == 2 && !HOMOG) ? 2 : LCV == 2 ? 3 : 4))
     walk4_kernel(const __grid_constant__ Walk4Params P4) {
-  constexpr int MP = 4, L = 4;
-  constexpr int G = 4 / LCV;                 // lanes per pattern
+  static_assert(LT % LCV == 0, "categories split evenly over a pattern's lanes");
+  constexpr int MP = 4, L = LT;
+  constexpr int G = LT / LCV;                // lanes per pattern
   constexpr int TP = 32 / G;                 // patterns per warp tile
   constexpr int TCB = L * NC * MP;           // doubles per node TC block
   constexpr int TCC = TCB / 2;               // double2 chunks per TC block

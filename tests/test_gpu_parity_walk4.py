@@ -108,3 +108,49 @@ def test_walk4_iupac_classes(lcv):
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
     assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+
+
+def _gtr(rng):
+    pi = rng.dirichlet(np.ones(4) * 5)
+    s = rng.lognormal(0, 0.5, (4, 4))
+    s = (s + s.T) / 2
+    q = s * pi[None, :]
+    np.fill_diagonal(q, 0)
+    np.fill_diagonal(q, -q.sum(1))
+    q /= -np.sum(pi * np.diag(q))
+    return q, pi
+
+
+@pytest.mark.parametrize("L", [1, 2])
+@pytest.mark.parametrize("homog", [True, False], ids=["homog", "per_branch_q"])
+def test_walk4_one_and_two_categories(L, homog):
+    """The pipelined kernel for models without / with a two-class rate mixture
+    (one lane per pattern), with gaps, per-branch generators and the Hessian."""
+    rng = np.random.default_rng(60 + L)
+    q, pi = _gtr(rng)
+    mo = O.Model(q, pi, True)
+    taxa = 40
+    tree_o = O.Tree.random(O.Rng(70 + L), taxa, 0.01, 0.2)
+    bq = [] if homog else _branch_q(9, 2 * taxa - 2, k=4)
+    for br, g in bq:
+        mo.set_branch_generator(br, g)
+    rates, probs = ([1.0], [1.0]) if L == 1 else O.discrete_gamma(0.6, 2)
+    codes = O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, 9000, 80 + L)
+    codes = np.where(rng.random(codes.shape) < 0.04, -1, codes)
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    ref = O.Engine(tree_o, O.Alignment.from_codes(codes, 4, labels), mo, rates, probs, blocks=16)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, tree_o.post_order)
+    model = SubstitutionModel(q, pi, True)
+    for br, g in bq:
+        model.set_branch_generator(br, g)
+    eng = LikelihoodEngine(tree, SitePatternAlignment.from_codes(labels, codes, 4), model,
+                           RateCategories(np.asarray(rates), np.asarray(probs)), EngineOptions())
+    for hess in (False, True):
+        ll, g, h = ref.branch_gradient(hess)
+        rep = eng.branch_gradient(hess)
+        assert eng.info()["kernel"] == "walk4_kernel"
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
+        if hess:
+            assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
