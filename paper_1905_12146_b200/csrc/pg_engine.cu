@@ -536,7 +536,14 @@ struct pg_engine {
     nc4 = MP == 4 ? pg_walk4_nc(NC) : 0;
     // pipelined 4-state kernel: 4 categories (one or two lanes per pattern) or
     // 1 / 2 categories (one lane per pattern)
-    use_walk4 = MP == 4 && G == 1 && LC == L && (L == 4 || L == 2 || L == 1) && !opt.capture_partials && nc4 > 0;
+    {
+      // L = 4 keeps its own lane split below; L = 1..3 use one lane per
+      // pattern, L = 8 two; every variant needs about one warp tile per SM
+      const int64_t tp = L == 8 ? 16 : 32;
+      use_walk4 = MP == 4 && !opt.capture_partials && nc4 > 0 && std::getenv("PG_NO_WALK4") == nullptr &&
+                  (L == 4 ? (LC == 4 && G == 1)
+                          : (L == 1 || ((L == 2 || L == 3 || L == 8) && int64_t(P) / tp >= int64_t(num_sms))));
+    }
     walk_smem = 0;
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
@@ -547,7 +554,7 @@ struct pg_engine {
         walk4_lcv = (int64_t(P) / 32 >= int64_t(num_sms) * 8 * 2) ? 4 : 2;
         if (const char* v = std::getenv("PG_WALK4_LCV")) walk4_lcv = std::atoi(v) == 4 ? 4 : 2;
       } else {
-        walk4_lcv = L;  // one lane per pattern holds every category
+        walk4_lcv = L == 8 ? 4 : L;  // one lane per pattern holds every category (L = 8: two lanes)
       }
       G = L / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);

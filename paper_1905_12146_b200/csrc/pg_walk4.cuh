@@ -64,7 +64,7 @@ __device__ __forceinline__ double pow2_neg(int ex) { return __hiloint2double((10
 // resident warps).
 template <bool HOMOG, bool HESS, int NC, int LCV, int LT = 4>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32,
-                                  (LCV == 4 || (LCV == 2 && LT == 2 && !HOMOG) ? 2 : LCV == 2 ? 3 : 4))
+                                  (LCV >= 3 || (LCV == 2 && LT == 2 && !HOMOG) ? 2 : LCV == 2 ? 3 : 4))
     walk4_kernel(const __grid_constant__ Walk4Params P4) {
   static_assert(LT % LCV == 0, "categories split evenly over a pattern's lanes");
   constexpr int MP = 4, L = LT;

@@ -121,11 +121,12 @@ def _gtr(rng):
     return q, pi
 
 
-@pytest.mark.parametrize("L", [1, 2])
+@pytest.mark.parametrize("L", [1, 2, 3, 8])
 @pytest.mark.parametrize("homog", [True, False], ids=["homog", "per_branch_q"])
-def test_walk4_one_and_two_categories(L, homog):
-    """The pipelined kernel for models without / with a two-class rate mixture
-    (one lane per pattern), with gaps, per-branch generators and the Hessian."""
+def test_walk4_other_category_counts(L, homog):
+    """The pipelined kernel for 1, 2, 3 rate categories (one lane per pattern)
+    and 8 (two lanes per pattern), with gaps, per-branch generators and the
+    Hessian."""
     rng = np.random.default_rng(60 + L)
     q, pi = _gtr(rng)
     mo = O.Model(q, pi, True)
@@ -134,7 +135,7 @@ def test_walk4_one_and_two_categories(L, homog):
     bq = [] if homog else _branch_q(9, 2 * taxa - 2, k=4)
     for br, g in bq:
         mo.set_branch_generator(br, g)
-    rates, probs = ([1.0], [1.0]) if L == 1 else O.discrete_gamma(0.6, 2)
+    rates, probs = ([1.0], [1.0]) if L == 1 else O.discrete_gamma(0.6, L)
     codes = O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, 9000, 80 + L)
     codes = np.where(rng.random(codes.shape) < 0.04, -1, codes)
     labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
