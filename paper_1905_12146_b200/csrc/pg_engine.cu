@@ -505,9 +505,11 @@ struct pg_engine {
   int walk_max_blocks_per_sm();
 
   void prepare_geometry() {
-    use_walkm = m > 8 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
+    // DMMA kernel for every state space above 4 (m = 5..8 on walkm<8>: 1.8x
+    // the generic kernel, scripts/m_scale.py)
+    use_walkm = m > 4 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
     if (use_walkm) {
-      MP = m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
+      MP = m <= 8 ? 8 : m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
       // walkm indexes its tables and per-warp scratch with 32-bit offsets
       const int64_t lim = int64_t(1) << 31;
       if (int64_t(B()) * L * (MP + A) * MP >= lim || int64_t(N) * L * MP * 32 >= lim) use_walkm = false;

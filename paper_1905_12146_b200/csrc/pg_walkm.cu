@@ -8,6 +8,7 @@ static void* pick(bool hess) {
 }
 
 void* pg_walkm_kernel(int mp, bool hess) {
+  if (mp == 8) return pick<8>(hess);
   if (mp == 16) return pick<16>(hess);
   if (mp == 20) return pick<20>(hess);
   if (mp == 24) return pick<24>(hess);
@@ -17,6 +18,7 @@ void* pg_walkm_kernel(int mp, bool hess) {
 }
 
 size_t pg_walkm_smem(int mp) {
+  if (mp == 8) return pgk::WalkMGeom<8>::smem_bytes();
   if (mp == 16) return pgk::WalkMGeom<16>::smem_bytes();
   if (mp == 20) return pgk::WalkMGeom<20>::smem_bytes();
   if (mp == 24) return pgk::WalkMGeom<24>::smem_bytes();
@@ -26,6 +28,7 @@ size_t pg_walkm_smem(int mp) {
 }
 
 int pg_walkm_wpc(int mp) {
+  if (mp == 8) return pgk::WalkMGeom<8>::WPC;
   if (mp == 16) return pgk::WalkMGeom<16>::WPC;
   if (mp == 20) return pgk::WalkMGeom<20>::WPC;
   if (mp == 24) return pgk::WalkMGeom<24>::WPC;

@@ -1,6 +1,5 @@
-"""GPU parity of every large-state (DMMA walkm) instantiation and of the
-engine routes, against the CPU oracle: MP = 16 / 20 (odd k-step chains) /
-24 / 32 / 64, one and many rate categories (operand staging on and off),
+"""GPU parity of every DMMA walkm instantiation and of the engine routes,
+against the CPU oracle: MP = 8 / 16 / 20 (odd k-step chains) / 24 / 32 / 64, one and many rate categories (operand staging on and off),
 per-branch generators (non-homogeneous Q, Padé path), ambiguous and missing
 tips, the likelihood-only route (engine.hpp:146-149) against the gradient
 route (test_engine.cpp:161: routes agree), and a traversal-order change
@@ -74,7 +73,7 @@ def _check(eng, ref, hess=True):
     return rep
 
 
-@pytest.mark.parametrize("m,L", [(9, 1), (12, 4), (16, 3), (17, 4), (19, 1), (20, 5), (21, 2), (24, 4), (25, 1),
+@pytest.mark.parametrize("m,L", [(5, 2), (7, 4), (8, 1), (9, 1), (12, 4), (16, 3), (17, 4), (19, 1), (20, 5), (21, 2), (24, 4), (25, 1),
                                  (31, 4), (33, 2), (48, 4), (64, 1), (64, 3)])
 def test_walkm_instantiations(m, L):
     eng, ref = _pair(m, L, 13, 300, 97 * m + L, gaps=0.05)
