@@ -128,7 +128,6 @@ struct pg_engine {
   bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
   int codes_mp = 0;        // MP the device tip codes' class columns are encoded for
   int walkm_wpc = 4;       // warps per CTA in walkm
-  DevBuf<int> d_eexp, d_qexp;
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
   size_t walk_smem = 0;
   bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
@@ -512,7 +511,7 @@ struct pg_engine {
       MP = m <= 8 ? 8 : m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
       // walkm indexes its tables and per-warp scratch with 32-bit offsets
       const int64_t lim = int64_t(1) << 31;
-      if (int64_t(B()) * L * (MP + A) * MP >= lim || int64_t(N) * L * MP * 32 >= lim) use_walkm = false;
+      if (int64_t(B()) * L * (MP + A) * MP >= lim || int64_t(N) * L * (MP * 8 + 4) * 4 >= lim) use_walkm = false;
     }
     if (!use_walkm) MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
@@ -573,7 +572,8 @@ struct pg_engine {
       walk_smem = pg_walkm_smem(MP);
     }
     const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : pgk::kWarpsPerBlock);
-    const size_t vec = use_walkm ? size_t(L) * 8 * MP : size_t(32) * LC * MP;
+    // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents
+    const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
     size_t free_b = 0, total_b = 0;
     PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -586,10 +586,6 @@ struct pg_engine {
     } else {
       TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
       TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
-    }
-    if (use_walkm) {
-      d_eexp.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * L * 8);
-      d_qexp.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * L * 8);
     }
     accw = 1 + 2 * B();
     d_escr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
@@ -854,8 +850,6 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   if (use_walkm) {
     pgk::WalkMParams pm{};
     pm.p = p;
-    pm.eexp = d_eexp.p;
-    pm.qexp = d_qexp.p;
     pm.fpp = d_fpp.p;
     pm.fpt = d_fpt.p;
     pm.fq = d_fq.p;

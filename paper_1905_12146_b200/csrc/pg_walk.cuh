@@ -85,7 +85,7 @@ struct WalkParams {
   const double* probs;   // [L]
   const int4* post;      // [nsteps] {k, c0, c1, 0} internal nodes, heavy-child-first post order
   const int4* pre;       // [nsteps] {k, c0, c1, next} reverse of post; next = following step's node if a child of k
-  double* escr;          // [TW][N-1][VEC] edge messages e_k of internal non-root nodes
+  double* escr;          // [TW][N-1][VEC] edge messages e_k of internal non-root nodes (walkm: + exponents per slot)
   double* qscr;          // [TW][N-1][VEC] pre-order partials of deferred internal nodes
   double* acc;           // [TW][accw]: [0] logL, [x] grad of branch x, [B+x] hess
   int* err;              // [2] first non-finite pattern, first underflowed pattern
@@ -110,8 +110,6 @@ struct Walk4Params {
 // Parameters of the DMMA large-state kernel (pg_walkm.cuh).
 struct WalkMParams {
   WalkParams p;
-  int* eexp;  // [TW][N-1][L][8] exponents of the stored edge messages
-  int* qexp;  // [TW][N-1][L][8] exponents of the stored pre-partials
   const double* fpp;  // [B][L][MP*MP] P in B-fragment order (y = P x)
   const double* fpt;  // [B][L][MP*MP] (y = P^T x)
   const double* fq;   // [nQ][MP*MP] generators in B-fragment order (y = Q x)

@@ -88,8 +88,11 @@ struct WalkMGeom {
   // C5: 8 warps with double-buffered 32 KB codon blocks (one CTA per SM) is
   // slower than two 4-warp CTAs (432 vs 423 ms).
   static constexpr int WPC = MP <= 32 ? PG_WALKM_WPC_SMALL : 4;
-  // per warp: 2 stages x 3 operands x K x 32 doubles + 2 x 3 x 32 exponents
-  static constexpr int SOPD = SOP ? (6 * K * 32 + 6 * 32 / 2) : 0;
+  // one (node, category) scratch slot: K x 32 doubles of the warp's 8 vectors
+  // followed by their 8 int exponents (one bulk copy moves both)
+  static constexpr int SL = K * 32 + 4;
+  // per warp: 2 stages x 3 operand slots
+  static constexpr int SOPD = SOP ? 6 * SL : 0;
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
   // + SOP + two mbarriers (one per buffer parity) for the bulk copies
   static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD + 2) * sizeof(double); }
@@ -155,11 +158,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   const int ntile_cta = (p.P + 8 * WPC - 1) / (8 * WPC);
   // 32-bit element offsets inside the per-warp scratch and the K1 tables
   // (the host guarantees they fit) keep the index math to one IMAD.WIDE
-  const int slotd = L * K * 32;  // doubles per node slot per warp
+  constexpr int SL = Gm::SL;
+  const int slotd = L * SL;  // doubles per node slot per warp
   double* E = p.escr + size_t(warp) * size_t(N - 1) * slotd;
   double* Qs = p.qscr + size_t(warp) * size_t(N - 1) * slotd;
-  int* Ex = PM.eexp + size_t(warp) * size_t(N - 1) * L * 8;
-  int* Qx = PM.qexp + size_t(warp) * size_t(N - 1) * L * 8;
   double* Acc = p.acc + size_t(warp) * p.accw;
   for (int i = lane; i < p.accw; i += 32) Acc[i] = 0.0;
   __syncwarp();
@@ -263,9 +265,12 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     const bool sop = Gm::SOP && L > 1;
 
     // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
-    // an odd last k-step as [lane] double
+    // an odd last k-step as [lane] double, then the 8 patterns' exponents
     auto slot_ptr = [&](const double* base, int node, int l) {
-      return reinterpret_cast<const double2*>(base + ((node - N - 1) * slotd + l * (K * 32))) + lane;
+      return reinterpret_cast<const double2*>(base + ((node - N - 1) * slotd + l * SL)) + lane;
+    };
+    auto xslot = [&](double* base, int node, int l) -> int* {
+      return reinterpret_cast<int*>(base + ((node - N - 1) * slotd + l * SL + K * 32)) + q;
     };
     auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
       const double2* src = slot_ptr(base, node, l);
@@ -286,17 +291,13 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // ---- staged operands (SOP): the next unit's operands are copied into a
     // per-warp shared stage (bulk copies for scratch slots, per-lane cp.async
     // gathers for tip columns) while this unit computes
-    auto opbuf = [&](int stage, int which) -> double* { return sop_base + (stage * 3 + which) * (K * 32); };
-    auto xpbuf = [&](int stage, int which) -> int* {
-      return reinterpret_cast<int*>(sop_base + 6 * (K * 32)) + (stage * 3 + which) * 32;
-    };
-    // the warp's whole slot (K x 32 doubles) and its 8 exponents: two bulk copies
-    auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l, const int* xsrc) {
+    auto opbuf = [&](int stage, int which) -> double* { return sop_base + (stage * 3 + which) * SL; };
+    auto xpbuf = [&](int stage, int which) -> int* { return reinterpret_cast<int*>(opbuf(stage, which) + K * 32); };
+    // the warp's whole slot (K x 32 doubles + its 8 exponents): one bulk copy
+    auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l) {
       if (lane == 0) {
-        bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * (K * 32)), K * 32 * sizeof(double),
-                 mbar + stage);
-        bulk_g2s(xpbuf(stage, which), xsrc - q, 8 * sizeof(int), mbar + stage);
-        txW += K * 32 * sizeof(double) + 8 * sizeof(int);
+        bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * SL), SL * sizeof(double), mbar + stage);
+        txW += SL * sizeof(double);
       }
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
@@ -329,7 +330,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
 #pragma unroll
       for (int ki = 0; ki < K; ++ki) v[ki] = __ldg(col + ki * 4);
     };
-    auto exp_idx = [&](int node, int l) { return ((node - N - 1) * L + l) * 8 + q; };
     auto tipcode = [&](int node) -> int { return node <= N ? int(codes[int64_t(node - 1) * Pc]) : 0; };
 
     // ------------------------------------------------ post-order pass (a)
@@ -342,12 +342,12 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (st.y <= N) gather(st.y, c0, l, a);
         else {
           load_slot(E, st.y, l, a);
-          xa = Ex[exp_idx(st.y, l)];
+          xa = *xslot(E, st.y, l);
         }
         if (st.z <= N) gather(st.z, c1, l, b);
         else {
           load_slot(E, st.z, l, b);
-          xb = Ex[exp_idx(st.z, l)];
+          xb = *xslot(E, st.z, l);
         }
       };
       int4 stc = p.post[0];
@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
       auto stage_post_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
         if (st.y <= N) stage_gather_op(stage, 0, st.y, c0, l);
-        else stage_slot_op(stage, 0, E, st.y, l, Ex + exp_idx(st.y, l));
+        else stage_slot_op(stage, 0, E, st.y, l);
         if (st.z <= N) stage_gather_op(stage, 1, st.z, c1, l);
-        else stage_slot_op(stage, 1, E, st.z, l, Ex + exp_idx(st.z, l));
+        else stage_slot_op(stage, 1, E, st.z, l);
       };
       if (PIPE && stc.x != root) stage_P(pbuf(0, 0), PM.fpp, stc.x, 0, 0);
       if (sop) stage_post_ops(stc, cc0, cc1, 0, 0);
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           double e[K];
           matvec_P(pbuf(0, par), a, e);
           store_slot(E, stc.x, l, e);
-          if (t == 0) Ex[exp_idx(stc.x, l)] = Sk;
+          if (t == 0) *xslot(E, stc.x, l) = Sk;
         }
         l = l2;
         if (step_end) {
@@ -458,15 +458,15 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
         } else {
           load_slot(Qs, st.x, l, qv);
-          xq = Qx[exp_idx(st.x, l)];
+          xq = *xslot(Qs, st.x, l);
         }
         if (st.y > N) {
           load_slot(E, st.y, l, ea);
-          xa = Ex[exp_idx(st.y, l)];
+          xa = *xslot(E, st.y, l);
         } else gather(st.y, c0, l, ea);
         if (st.z > N) {
           load_slot(E, st.z, l, eb);
-          xb = Ex[exp_idx(st.z, l)];
+          xb = *xslot(E, st.z, l);
         } else gather(st.z, c1, l, eb);
       };
       auto stage_pre = [&](const int4 st, int l, int par) {
@@ -482,10 +482,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       int cc0 = tipcode(stc.y), cc1 = tipcode(stc.z);
       int cn0 = tipcode(stn.y), cn1 = tipcode(stn.z);
       auto stage_pre_ops = [&](const int4 st, int c0, int c1, int l, int stage) {
-        if (st.x != root) stage_slot_op(stage, 2, Qs, st.x, l, Qx + exp_idx(st.x, l));
-        if (st.y > N) stage_slot_op(stage, 0, E, st.y, l, Ex + exp_idx(st.y, l));
+        if (st.x != root) stage_slot_op(stage, 2, Qs, st.x, l);
+        if (st.y > N) stage_slot_op(stage, 0, E, st.y, l);
         else stage_gather_op(stage, 0, st.y, c0, l);
-        if (st.z > N) stage_slot_op(stage, 1, E, st.z, l, Ex + exp_idx(st.z, l));
+        if (st.z > N) stage_slot_op(stage, 1, E, st.z, l);
         else stage_gather_op(stage, 1, st.z, c1, l);
       };
       if (PIPE) stage_pre(stc, 0, 0);
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           const int ex = quad_peak_exp(qo);
           scale_by(qo, ex);
           store_slot(Qs, x, l, qo);
-          if (t == 0) Qx[exp_idx(x, l)] = xbase + ex;
+          if (t == 0) *xslot(Qs, x, l) = xbase + ex;
         };
         if (a_int) {
           double qo[K];
