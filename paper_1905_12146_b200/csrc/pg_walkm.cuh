@@ -104,6 +104,9 @@ template <int MP, bool HESS>
 __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_MINB_SMALL : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
+  // lane 0 of the last warp issues the P-block copies (warps 0..2 issue the
+  // staged operand slots), spreading the copy issue over the CTA's warps
+  constexpr int kPIssuer = 32 * (Gm::WPC - 1);
   // (measured and removed: register prefetch of the next unit's operands,
   // interleaved mat-vecs of the two children -- both cost registers at the
   // 128-register cap of 4 CTAs per SM)
@@ -113,12 +116,13 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   extern __shared__ __align__(16) double smd[];
   auto pbuf = [&](int slot, int par) -> double* { return smd + size_t(PIPE ? slot * 2 + par : slot) * FRAG; };
   double* Qsm = smd + size_t(Gm::NPB) * FRAG;  // homogeneous generator in B-fragment order
-  double* sop_base = smd + size_t(Gm::NPB + 1) * FRAG + size_t(threadIdx.x >> 5) * Gm::SOPD;
+  // staged operands of the whole CTA: [stage][operand][warp][slot]
+  double* sop_cta = smd + size_t(Gm::NPB + 1) * FRAG;
   // P blocks and operand slots are staged with 1-D bulk copies (TMA engine)
   // that complete on these mbarriers
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smd + size_t(Gm::NPB + 1) * FRAG + size_t(Gm::WPC) * Gm::SOPD);
   if (threadIdx.x == 0) {
-    mbar_init(mbar, Gm::WPC + 1);  // lane 0 of every warp + thread 0 (P blocks)
+    mbar_init(mbar, Gm::WPC + 1);  // lane 0 of every warp + the P-block issuer
     mbar_init(mbar + 1, Gm::WPC + 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // all staging for a buffer is issued: arm its mbarrier with the bytes
   auto stage_done = [&](int sb) {
     if ((threadIdx.x & 31) == 0) mbar_arrive_tx(mbar + sb, txW);
-    if (threadIdx.x == 0) mbar_arrive_tx(mbar + sb, txP);
+    if (threadIdx.x == kPIssuer) mbar_arrive_tx(mbar + sb, txP);
     txP = txW = 0;
   };
   // wait for a buffer's bulk copies (and every thread's cp.async), then the
@@ -159,16 +163,18 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   // 32-bit element offsets inside the per-warp scratch and the K1 tables
   // (the host guarantees they fit) keep the index math to one IMAD.WIDE
   constexpr int SL = Gm::SL;
-  const int slotd = L * SL;  // doubles per node slot per warp
-  double* E = p.escr + size_t(warp) * size_t(N - 1) * slotd;
-  double* Qs = p.qscr + size_t(warp) * size_t(N - 1) * slotd;
+  // CTA-major scratch: [CTA][node][category][warp][slot], so one (node,
+  // category) operand of the whole lock-step CTA is one contiguous bulk copy
+  const int slotd = L * WPC * SL;  // doubles per node of the CTA
+  double* E = p.escr + size_t(blockIdx.x) * size_t(N - 1) * slotd;
+  double* Qs = p.qscr + size_t(blockIdx.x) * size_t(N - 1) * slotd;
   double* Acc = p.acc + size_t(warp) * p.accw;
   for (int i = lane; i < p.accw; i += 32) Acc[i] = 0.0;
   __syncwarp();
 
   // stage one (node, category) matrix in B-fragment order (contiguous copy)
   auto stage_P = [&](double* buf, const double* tab, int node, int l, int sb) {
-    if (tid == 0) {
+    if (tid == kPIssuer) {
       bulk_g2s(buf, tab + ((node - 1) * L + l) * FRAG, FRAG * sizeof(double), mbar + sb);
       txP += FRAG * sizeof(double);
     }
@@ -267,10 +273,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
     // an odd last k-step as [lane] double, then the 8 patterns' exponents
     auto slot_ptr = [&](const double* base, int node, int l) {
-      return reinterpret_cast<const double2*>(base + ((node - N - 1) * slotd + l * SL)) + lane;
+      return reinterpret_cast<const double2*>(base + ((node - N - 1) * slotd + (l * WPC + wib) * SL)) + lane;
     };
     auto xslot = [&](double* base, int node, int l) -> int* {
-      return reinterpret_cast<int*>(base + ((node - N - 1) * slotd + l * SL + K * 32)) + q;
+      return reinterpret_cast<int*>(base + ((node - N - 1) * slotd + (l * WPC + wib) * SL + K * 32)) + q;
     };
     auto load_slot = [&](const double* base, int node, int l, double (&v)[K]) {
       const double2* src = slot_ptr(base, node, l);
@@ -291,13 +297,15 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // ---- staged operands (SOP): the next unit's operands are copied into a
     // per-warp shared stage (bulk copies for scratch slots, per-lane cp.async
     // gathers for tip columns) while this unit computes
-    auto opbuf = [&](int stage, int which) -> double* { return sop_base + (stage * 3 + which) * SL; };
+    auto opbuf = [&](int stage, int which) -> double* { return sop_cta + ((stage * 3 + which) * WPC + wib) * SL; };
     auto xpbuf = [&](int stage, int which) -> int* { return reinterpret_cast<int*>(opbuf(stage, which) + K * 32); };
-    // the warp's whole slot (K x 32 doubles + its 8 exponents): one bulk copy
+    // the CTA's slots of one operand (WPC x (K x 32 doubles + 8 exponents)):
+    // one bulk copy, issued by lane 0 of warp `which` (operands spread over warps)
     auto stage_slot_op = [&](int stage, int which, const double* base, int node, int l) {
-      if (lane == 0) {
-        bulk_g2s(opbuf(stage, which), base + ((node - N - 1) * slotd + l * SL), SL * sizeof(double), mbar + stage);
-        txW += SL * sizeof(double);
+      if (lane == 0 && wib == which % WPC) {
+        bulk_g2s(sop_cta + (stage * 3 + which) * WPC * SL, base + ((node - N - 1) * slotd + l * WPC * SL),
+                 WPC * SL * sizeof(double), mbar + stage);
+        txW += WPC * SL * sizeof(double);
       }
     };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
