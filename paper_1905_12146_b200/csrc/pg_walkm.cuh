@@ -477,9 +477,27 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           xb = *xslot(E, st.z, l);
         } else gather(st.z, c1, l, eb);
       };
+      // a tip child has no outgoing pre-partial, so its P^T buffer instead
+      // receives the child's Q P column table (NC x MP) when it fits: the
+      // tip's Q e is then a shared-memory read instead of a dependent global
+      // gather in the middle of the unit
+      const bool qstage = PIPE && NC * MP <= FRAG;
+      auto stage_qtc = [&](double* buf, int node, int l, int sb) {
+        if (tid == kPIssuer) {
+          bulk_g2s(buf, p.qtc + size_t((node - 1) * L + l) * (NC * MP), NC * MP * sizeof(double), mbar + sb);
+          txP += NC * MP * sizeof(double);
+        }
+      };
       auto stage_pre = [&](const int4 st, int l, int par) {
         if (st.y > N) stage_P(pbuf(0, par), PM.fpt, st.y, l, par);
+        else if (qstage) stage_qtc(pbuf(0, par), st.y, l, par);
         if (st.z > N) stage_P(pbuf(1, par), PM.fpt, st.z, l, par);
+        else if (qstage) stage_qtc(pbuf(1, par), st.z, l, par);
+      };
+      auto staged_q = [&](const double* buf, int code, double (&v)[K]) {
+        const double* col = buf + code * MP + t;
+#pragma unroll
+        for (int ki = 0; ki < K; ++ki) v[ki] = col[ki * 4];
       };
       int4 stc = p.pre[0];
       int4 stn = n > 1 ? p.pre[1] : stc;
@@ -554,8 +572,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         {
           double ua[K], ub[K];
           if (a_int) matvec_Q(Qa, ea, ua);
+          else if (qstage) staged_q(pbuf(0, par), cc0, ua);
           else gather_q(ca, cc0, l, ua);
           if (b_int) matvec_Q(Qb, eb, ub);
+          else if (qstage) staged_q(pbuf(1, par), cc1, ub);
           else gather_q(cb, cc1, l, ub);
           double d1a = 0.0, d1b = 0.0;
 #pragma unroll
