@@ -308,7 +308,20 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         txW += WPC * SL * sizeof(double);
       }
     };
+    // a tip operand: the child's whole column table (NC x MP) is one bulk copy
+    // into the operand's CTA region when it fits (each lane then reads its
+    // pattern's column); otherwise per-lane 8-byte gathers of the column
+    const bool tstage = Gm::SOP && NC * MP <= WPC * SL;
+    auto opblk = [&](int stage, int which) -> double* { return sop_cta + (stage * 3 + which) * WPC * SL; };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
+      if (tstage) {
+        if (lane == 0 && wib == which % WPC) {
+          bulk_g2s(opblk(stage, which), p.tc + size_t((node - 1) * L + l) * (NC * MP), NC * MP * sizeof(double),
+                   mbar + stage);
+          txW += NC * MP * sizeof(double);
+        }
+        return;
+      }
       const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
       double* dst = opbuf(stage, which);
 #pragma unroll
@@ -326,6 +339,12 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       }
       if constexpr (K & 1) v[K - 1] = reinterpret_cast<const double*>(src - lane + (K / 2) * 32)[lane];
       x = xpbuf(stage, which)[q];
+    };
+    auto read_tip = [&](int stage, int which, int code, double (&v)[K], int& x) {
+      const double* col = opblk(stage, which) + code * MP + t;
+#pragma unroll
+      for (int ki = 0; ki < K; ++ki) v[ki] = col[ki * 4];
+      x = 0;
     };
     auto gather = [&](int node, int code, int l, double (&v)[K]) {
       const double* col = p.tc + (((node - 1) * L + l) * NC + code) * MP + t;
@@ -400,8 +419,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         double a[K], b[K];
         int xa = 0, xb = 0;
         if (sop) {
-          read_op(u & 1, 0, a, xa);
-          read_op(u & 1, 1, b, xb);
+          if (tstage && stc.y <= N) read_tip(u & 1, 0, cc0, a, xa);
+          else read_op(u & 1, 0, a, xa);
+          if (tstage && stc.z <= N) read_tip(u & 1, 1, cc1, b, xb);
+          else read_op(u & 1, 1, b, xb);
         } else {
           load_post(stc, cc0, cc1, l, a, b, xa, xb);
         }
@@ -551,8 +572,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           } else {
             read_op(u & 1, 2, qv, xq);
           }
-          read_op(u & 1, 0, ea, xa);
-          read_op(u & 1, 1, eb, xb);
+          if (tstage && !a_int) read_tip(u & 1, 0, cc0, ea, xa);
+          else read_op(u & 1, 0, ea, xa);
+          if (tstage && !b_int) read_tip(u & 1, 1, cc1, eb, xb);
+          else read_op(u & 1, 1, eb, xb);
         } else {
           load_pre(stc, cc0, cc1, l, qv, ea, eb, xq, xa, xb);
         }
