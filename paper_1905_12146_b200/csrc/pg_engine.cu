@@ -482,9 +482,8 @@ struct pg_engine {
         for (int e = 0; e < frag; ++e) {
           const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
           const int k = 4 * ki + (lane & 3), gq = lane >> 2, n = 4 * (2 * ni + (gq & 1)) + (gq >> 1);
-          if (n < MP) fq[size_t(g) * frag + e] = qt[size_t(g) * MP * MP + size_t(n) * MP + k];
+          if (n < MP) fq[size_t(g) * frag + pgk::frag_pos(f, lane, KK * NT)] = qt[size_t(g) * MP * MP + size_t(n) * MP + k];
         }
-      (void)KK;
       d_fq.upload(fq.data(), fq.size(), stream);
     }
     d_qidx.upload(qidx.data(), qidx.size(), stream);

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pg_walk.cuh"  // frag_pos
+
 namespace pgk {
 
 // Fixed-order reduction over warps (deterministic for a fixed grid), plus the
@@ -252,8 +254,9 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
       const int lane = e & 31, f = e >> 5, ki = f / NT, ni = f % NT;
       const int k = 4 * ki + (lane & 3), g = lane >> 2, n = 4 * (2 * ni + (g & 1)) + (g >> 1);
       const bool in = k < m && n < m;
-      fp[e] = in ? R[n * m + k] : 0.0;  // y = P x: M(k, n) = P[n][k]
-      ft[e] = in ? R[k * m + n] : 0.0;  // y = P^T x: M(k, n) = P[k][n]
+      const int at = frag_pos(f, lane, KK * NT);
+      fp[at] = in ? R[n * m + k] : 0.0;  // y = P x: M(k, n) = P[n][k]
+      ft[at] = in ? R[k * m + n] : 0.0;  // y = P^T x: M(k, n) = P[k][n]
     }
   }
   if (p.qtc) {

@@ -73,6 +73,18 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Storage position of B fragment f = ki * NT + ni (of F = K * NT) for `lane`
+// in the walkm matrix tables.  Codon-size tables (F >= kFragPairMin) store the
+// fragments in pairs, (2h, 2h+1) adjacent per lane, so one 16-byte
+// shared-memory load feeds two DMMAs (C5 413 -> 397 ms); an odd last fragment
+// follows the pairs lane-contiguously.  Smaller tables keep one fragment per
+// 256-byte row (C4: 144.6 vs 146.3 ms paired).
+constexpr int kFragPairMin = 64;
+__host__ __device__ __forceinline__ int frag_pos(int f, int lane, int F) {
+  if (F < kFragPairMin) return f * 32 + lane;
+  return f < (F & ~1) ? (((f >> 1) * 32 + lane) * 2 + (f & 1)) : ((F >> 1) * 64 + lane);
+}
+
 struct WalkParams {
   const uint8_t* codes;  // [N][Pc] tip column index into the TC table (rows padded to 32)
   const double* weights; // [P]

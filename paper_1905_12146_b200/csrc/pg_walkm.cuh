@@ -38,28 +38,34 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 // D (8 patterns x 8 NT states) = x^T M over K k-steps, one accumulator chain
 // per n-tile (NT independent chains in flight; the other resident warps cover
 // the 26-cycle dependent-DMMA latency, profiles/dmma_latency_b200.jsonl).
-template <int K, int NT, class F>
-__device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT][2], F bfrag) {
-  // one accumulator chain per n-tile: at the 128-register cap the even/odd
-  // k-step split costs more than it hides (C4 176 vs 179 ms)
-  constexpr int NSPLIT = 1;
-  double acc[NSPLIT][NT][2];
+// Codon-size tables store B fragments in pairs (frag_pos): one 16-byte load
+// per two DMMAs.
+// (measured and removed: an even/odd k-step accumulator split, C4 176 vs 179 ms)
+template <int K, int NT, bool GLOBAL>
+__device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT][2], const double* frag, int lane) {
+  constexpr int F = K * NT;
 #pragma unroll
-  for (int h = 0; h < NSPLIT; ++h)
+  for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
+  if constexpr (F < kFragPairMin) {
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) acc[h][ni][0] = acc[h][ni][1] = 0.0;
-#pragma unroll
-  for (int ki = 0; ki < K; ++ki)
-#pragma unroll
-    for (int ni = 0; ni < NT; ++ni) dmma(acc[ki % NSPLIT][ni][0], acc[ki % NSPLIT][ni][1], x[ki], bfrag(ki, ni));
-#pragma unroll
-  for (int ni = 0; ni < NT; ++ni) {
-    d[ni][0] = acc[0][ni][0];
-    d[ni][1] = acc[0][ni][1];
-    if constexpr (NSPLIT == 2) {
-      d[ni][0] += acc[NSPLIT - 1][ni][0];
-      d[ni][1] += acc[NSPLIT - 1][ni][1];
+    for (int f = 0; f < F; ++f) {
+      const double* fp = frag + f * 32 + lane;
+      dmma(d[f % NT][0], d[f % NT][1], x[f / NT], GLOBAL ? __ldg(fp) : *fp);
     }
+    return;
+  }
+  const double2* f2 = reinterpret_cast<const double2*>(frag) + lane;
+#pragma unroll
+  for (int h = 0; h < F / 2; ++h) {
+    const double2 b = GLOBAL ? __ldg(f2 + h * 32) : f2[h * 32];
+    const int f0 = 2 * h, f1 = 2 * h + 1;
+    dmma(d[f0 % NT][0], d[f0 % NT][1], x[f0 / NT], b.x);
+    dmma(d[f1 % NT][0], d[f1 % NT][1], x[f1 / NT], b.y);
+  }
+  if constexpr (F & 1) {
+    const double* f1p = frag + (F / 2) * 64 + lane;
+    const double b = GLOBAL ? __ldg(f1p) : *f1p;
+    dmma(d[(F - 1) % NT][0], d[(F - 1) % NT][1], x[(F - 1) / NT], b);
   }
 }
 
@@ -180,11 +186,11 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     }
   };
   // y = M x over the warp's 8 patterns: B fragment (ki, ni) for this lane is
-  // frag[(ki * NT + ni) * 32 + lane]; with the permuted columns baked into the
+  // frag[frag_pos(ki * NT + ni, lane, K * NT)]; with the permuted columns baked into the
   // fragment tables, D tile ni holds y's A-layout entries 2ni and 2ni+1.
   auto matvec = [&](const double* frag, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
-    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return frag[(ki * NT + ni) * 32 + lane]; });
+    dmma_chain<K, NT, false>(x, d, frag, lane);
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       y[2 * ni] = d[ni][0];
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   };
   auto matvec_g = [&](const double* frag, const double (&x)[K], double (&y)[K]) {
     double d[NT][2];
-    dmma_chain<K, NT>(x, d, [&](int ki, int ni) { return __ldg(frag + (ki * NT + ni) * 32 + lane); });
+    dmma_chain<K, NT, true>(x, d, frag, lane);
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) {
       y[2 * ni] = d[ni][0];
