@@ -115,6 +115,8 @@ class ClockSampler:
         self.period = period_ms
         self.samples = []
         self.proc = None
+        self.first = 0
+        self.after = False
 
     def __enter__(self):
         if self.period <= 0:
@@ -128,6 +130,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # the sampler is live before the region starts (nvidia-smi start-up
+            # takes longer than a short region)
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 10:
+                time.sleep(0.005)
+            self.first = len(self.samples)
         except Exception:
             self.proc = None
         return self
@@ -140,6 +148,13 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            n = len(self.samples)
+            # a region shorter than the period: keep the first sample taken after it
+            t0 = time.time()
+            while n <= self.first and len(self.samples) <= self.first and time.time() - t0 < 2:
+                time.sleep(0.002)
+            self.after = n <= self.first
+            self.samples = self.samples[self.first:self.first + 1] if self.after else self.samples[self.first:n]
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -158,7 +173,8 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                **({"note": "region shorter than the sampling period: first sample after it"} if self.after else {})}
 
 
 def cpu_baseline(inst, sample, threads, target_s=10.0):
