@@ -229,3 +229,35 @@ def test_extreme_branch_lengths(m):
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
     assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+
+
+@pytest.mark.parametrize("m,L,A", [(20, 4, 2), (20, 4, 6), (20, 4, 14), (12, 4, 3), (16, 2, 1), (24, 4, 5),
+                                   (32, 3, 2), (61, 2, 3)])
+def test_walkm_ambiguity_classes_table_staging(m, L, A):
+    """Tip column tables (NC = MP + A columns) are bulk-copied into shared
+    memory when they fit (P x and Q P tables; pg_walkm.cuh `tstage`,
+    `qstage`) and gathered per lane otherwise: class counts on both sides of
+    each limit, every tip code kind (state, missing, class) mixed."""
+    rng = np.random.default_rng(1000 * m + 10 * L + A)
+    q, pi = _reversible(m, rng)
+    mo = O.Model(q, pi, True)
+    r = O.Rng(m + A)
+    tree_o = O.Tree.random(r, 11, 0.03, 0.8)
+    rates, probs = O.discrete_gamma(0.5, L) if L > 1 else ([1.0], [1.0])
+    sites = 157
+    codes = np.asarray(O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, sites, 5 + m))
+    u = rng.random(codes.shape)
+    codes = np.where(u < 0.15, m + rng.integers(0, A, codes.shape), codes)
+    codes = np.where(u > 0.95, -1, codes)
+    amb = (rng.random((A, m)) < 0.3).astype(np.float64)
+    amb[:, 0] = 1.0  # every class admits at least one state
+    w = rng.integers(1, 4, sites)
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    ref = O.Engine(tree_o, O.Alignment.from_patterns(codes, m, w, amb, labels), mo, rates, probs)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, tree_o.post_order)
+    aln = SitePatternAlignment(labels, m, codes, w, amb)
+    eng = LikelihoodEngine(tree, aln, SubstitutionModel(q, pi, True),
+                           RateCategories(np.asarray(rates), np.asarray(probs)))
+    _check(eng, ref)
+    assert eng.info()["kernel"] == "walkm_kernel"
