@@ -670,7 +670,7 @@ struct pg_engine {
     if (te) PG_CUDA(cudaEventRecord(te[2], stream));
     const int width = want_hess ? accw : 1 + B();
     double* out = out_device ? out_device : d_out.p;
-    pgk::reduce_kernel<<<(width + 255) / 256, 256, 0, stream>>>(
+    pgk::reduce_kernel<<<(width + 31) / 32, 32 * pgk::kReduceGroups, 0, stream>>>(
         d_acc.p, TW, accw, width, out, (flags & PG_EVAL_RATE_GRAD) ? d_dt.p : nullptr, B());
     PG_CUDA(cudaGetLastError());
     ++launches;

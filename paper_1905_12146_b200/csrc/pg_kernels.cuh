@@ -11,20 +11,37 @@ namespace pgk {
 
 // Fixed-order reduction over warps (deterministic for a fixed grid), plus the
 // clock chain rule: d/dr_i = dt_i d/db_i, d2/dr_i2 = dt_i^2 d2/db_i2.
-__global__ void reduce_kernel(const double* __restrict__ acc, int TW, int accw, int width, double* __restrict__ out,
-                              const double* __restrict__ dt, int B) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= width) return;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int w = 0;
-  for (; w + 3 < TW; w += 4) {
-    s0 += acc[size_t(w) * accw + i];
-    s1 += acc[size_t(w + 1) * accw + i];
-    s2 += acc[size_t(w + 2) * accw + i];
-    s3 += acc[size_t(w + 3) * accw + i];
+// Block = 32 columns x kReduceGroups row groups: group r sums rows r, r + G,
+// r + 2G, ... (coalesced 256-byte row segments, four independent chains),
+// then the G partials are added in group order.  One thread per column
+// summing all rows serially was latency-bound (C2: 163 us of a 1.56 ms
+// evaluation).
+constexpr int kReduceGroups = 16;
+__global__ void __launch_bounds__(32 * kReduceGroups) reduce_kernel(const double* __restrict__ acc, int TW, int accw,
+                                                                   int width, double* __restrict__ out,
+                                                                   const double* __restrict__ dt, int B) {
+  __shared__ double part[kReduceGroups][33];
+  const int c = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + c;
+  double s = 0.0;
+  if (i < width) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int w = r;
+    constexpr int G = kReduceGroups;
+    for (; w + 3 * G < TW; w += 4 * G) {
+      s0 += acc[size_t(w) * accw + i];
+      s1 += acc[size_t(w + G) * accw + i];
+      s2 += acc[size_t(w + 2 * G) * accw + i];
+      s3 += acc[size_t(w + 3 * G) * accw + i];
+    }
+    for (; w < TW; w += G) s0 += acc[size_t(w) * accw + i];
+    s = (s0 + s1) + (s2 + s3);
   }
-  for (; w < TW; ++w) s0 += acc[size_t(w) * accw + i];
-  double s = (s0 + s1) + (s2 + s3);
+  part[r][c] = s;
+  __syncthreads();
+  if (r != 0 || i >= width) return;
+#pragma unroll
+  for (int g = 1; g < kReduceGroups; ++g) s += part[g][c];
   if (dt) {
     if (i >= 1 && i <= B) s *= dt[i - 1];
     else if (i > B) s *= dt[i - B - 1] * dt[i - B - 1];
