@@ -464,6 +464,11 @@ def main():
             cpu_value, how = cpu_baseline(inst, sample, threads, args.cpu_seconds)
             line["cpu_baseline"] = {"value": cpu_value, "unit": "pattern-branch/s", "cores": threads, "kind": "port",
                                     "sample": f"full tree, invalidate+gradient: {how}; {cpu_model()}"}
+            if threads > 1:
+                # SURVEY.md §8d variant (i): one thread, like the reference engine
+                # (engine.hpp:13-17), on a quarter of the sample
+                v1, how1 = cpu_baseline(inst, max(8, sample // 4), 1, min(args.cpu_seconds, 4.0))
+                line["cpu_baseline"]["single_thread"] = {"value": v1, "cores": 1, "sample": how1}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
