@@ -18,6 +18,8 @@
 //    (fire-and-forget, single writer per address -> deterministic).
 #pragma once
 
+#include <type_traits>
+
 #include "pg_walk.cuh"
 
 namespace pgk {
@@ -365,86 +367,104 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
         int ha = 0, hb = 0;
         const double* Ta = tcp(st, 0);
         const double* Tb = tcp(st, 1);
+        // the category loop, compiled per child kind (internal / tip) for
+        // LCV <= 2 so its operand selection and outgoing-partial code carry no
+        // branches (C2 1.48 -> 1.36 ms); one lane per pattern (LCV = 4) keeps
+        // one copy with runtime tests (C3 154 vs 157 ms specialised)
+        auto cat_loop = [&](auto ai, auto bi) {
+          const bool AI = ai, BI = bi;  // compile-time constants when given as std::integral_constant
 #pragma unroll
-        for (int j = 0; j < LCV; ++j) {
-          double q[4], ea[4], eb[4];
-          if (d.x == root) {
+          for (int j = 0; j < LCV; ++j) {
+            double q[4], ea[4], eb[4];
+            if (d.x == root) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) q[r] = P4.pi[r];
-          } else if (q_in_reg) {
+              for (int r = 0; r < 4; ++r) q[r] = P4.pi[r];
+            } else if (q_in_reg) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) q[r] = qreg[j][r];
-          } else {
-            read_cat(opp(st, 2), j, q);
-          }
-          if (a_int) read_cat(opp(st, 0), j, ea);
-          else gather_cat(Ta, code0, j, ea);
-          if (b_int) read_cat(opp(st, 1), j, eb);
-          else gather_cat(Tb, code1, j, eb);
-          double ta[4], tb[4], dd = 0.0;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            ta[r] = q[r] * eb[r];  // top for child a
-            tb[r] = q[r] * ea[r];  // top for child b
-            dd = fma(ta[r], ea[r], dd);
-          }
-          den = fma(cw[j], dd, den);
-          // gradient numerators: top . (Q e), Hessian: top . (Q^2 e)
-          double qea[4], qeb[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            double u = 0.0, v = 0.0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              u = fma(qm(d.y, r, c), ea[c], u);
-              v = fma(qm(d.z, r, c), eb[c], v);
+              for (int r = 0; r < 4; ++r) q[r] = qreg[j][r];
+            } else {
+              read_cat(opp(st, 2), j, q);
             }
-            qea[r] = u;
-            qeb[r] = v;
-          }
-          double d1a = 0.0, d1b = 0.0;
+            if (AI) read_cat(opp(st, 0), j, ea);
+            else gather_cat(Ta, code0, j, ea);
+            if (BI) read_cat(opp(st, 1), j, eb);
+            else gather_cat(Tb, code1, j, eb);
+            double ta[4], tb[4], dd = 0.0;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            d1a = fma(ta[r], qea[r], d1a);
-            d1b = fma(tb[r], qeb[r], d1b);
-          }
-          na = fma(crw[j], d1a, na);
-          nb = fma(crw[j], d1b, nb);
-          if constexpr (HESS) {
-            double d2a = 0.0, d2b = 0.0;
+            for (int r = 0; r < 4; ++r) {
+              ta[r] = q[r] * eb[r];  // top for child a
+              tb[r] = q[r] * ea[r];  // top for child b
+              dd = fma(ta[r], ea[r], dd);
+            }
+            den = fma(cw[j], dd, den);
+            // gradient numerators: top . (Q e), Hessian: top . (Q^2 e)
+            double qea[4], qeb[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               double u = 0.0, v = 0.0;
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-                u = fma(qm(d.y, r, c), qea[c], u);
-                v = fma(qm(d.z, r, c), qeb[c], v);
+                u = fma(qm(d.y, r, c), ea[c], u);
+                v = fma(qm(d.z, r, c), eb[c], v);
               }
-              d2a = fma(ta[r], u, d2a);
-              d2b = fma(tb[r], v, d2b);
+              qea[r] = u;
+              qeb[r] = v;
             }
-            na2 = fma(cr2w[j], d2a, na2);
-            nb2 = fma(cr2w[j], d2b, nb2);
-          }
-          // outgoing pre-partials q_x = P_x^T top (engine.hpp:249-250)
-          if (a_int) {
-            const double2* Tl = reinterpret_cast<const double2*>(Ta + (g * LCV + j) * NC * MP);
+            double d1a = 0.0, d1b = 0.0;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
-              qa[j][c] = fma(u.x, ta[0], fma(u.y, ta[1], fma(v.x, ta[2], v.y * ta[3])));
-              ha = max(ha, __double2hiint(qa[j][c]));
+            for (int r = 0; r < 4; ++r) {
+              d1a = fma(ta[r], qea[r], d1a);
+              d1b = fma(tb[r], qeb[r], d1b);
             }
-          }
-          if (b_int) {
-            const double2* Tl = reinterpret_cast<const double2*>(Tb + (g * LCV + j) * NC * MP);
+            na = fma(crw[j], d1a, na);
+            nb = fma(crw[j], d1b, nb);
+            if constexpr (HESS) {
+              double d2a = 0.0, d2b = 0.0;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
-              qb[j][c] = fma(u.x, tb[0], fma(u.y, tb[1], fma(v.x, tb[2], v.y * tb[3])));
-              hb = max(hb, __double2hiint(qb[j][c]));
+              for (int r = 0; r < 4; ++r) {
+                double u = 0.0, v = 0.0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  u = fma(qm(d.y, r, c), qea[c], u);
+                  v = fma(qm(d.z, r, c), qeb[c], v);
+                }
+                d2a = fma(ta[r], u, d2a);
+                d2b = fma(tb[r], v, d2b);
+              }
+              na2 = fma(cr2w[j], d2a, na2);
+              nb2 = fma(cr2w[j], d2b, nb2);
+            }
+            // outgoing pre-partials q_x = P_x^T top (engine.hpp:249-250)
+            if (AI) {
+              const double2* Tl = reinterpret_cast<const double2*>(Ta + (g * LCV + j) * NC * MP);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
+                qa[j][c] = fma(u.x, ta[0], fma(u.y, ta[1], fma(v.x, ta[2], v.y * ta[3])));
+                ha = max(ha, __double2hiint(qa[j][c]));
+              }
+            }
+            if (BI) {
+              const double2* Tl = reinterpret_cast<const double2*>(Tb + (g * LCV + j) * NC * MP);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
+                qb[j][c] = fma(u.x, tb[0], fma(u.y, tb[1], fma(v.x, tb[2], v.y * tb[3])));
+                hb = max(hb, __double2hiint(qb[j][c]));
+              }
             }
           }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if constexpr (LCV >= 4) {
+          cat_loop(a_int, b_int);
+        } else if (a_int) {
+          if (b_int) cat_loop(T_{}, T_{});
+          else cat_loop(T_{}, F_{});
+        } else {
+          if (b_int) cat_loop(F_{}, T_{});
+          else cat_loop(F_{}, F_{});
         }
         den = gsum(den);
         na = gsum(na);
