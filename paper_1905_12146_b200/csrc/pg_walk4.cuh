@@ -231,23 +231,70 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
         // p_k = e_c0 o e_c1 for all categories, then exponent normalisation
         double x[LCV][4];
         int hm = 0;
+        // child operand kinds: 0 tip (column gather), 1 the previous step's
+        // edge message (registers), 2 staged slot.  In the heavy-child-first
+        // order an internal child is either the previous step's node or its
+        // sibling is, so (tip, tip), (tip, kept), (kept, tip), (kept, slot)
+        // and (slot, kept) are the only combinations; for LCV <= 2 the loop
+        // is compiled per combination (no operand branches)
+        auto cat_loop = [&](auto ka, auto kb) {
+          const int KA = ka, KB = kb;
 #pragma unroll
-        for (int j = 0; j < LCV; ++j) {
-          double a[4], b[4];
-          if (d.y <= N) gather_cat(tcp(st, 1), code0, j, a);
-          else if (d.y == last) {
+          for (int j = 0; j < LCV; ++j) {
+            double a[4], b[4];
+            if (KA == 0) gather_cat(tcp(st, 1), code0, j, a);
+            else if (KA == 1) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = keep[j][r];
-          } else read_cat(opp(st, 0), j, a);
-          if (d.z <= N) gather_cat(tcp(st, 2), code1, j, b);
-          else if (d.z == last) {
+              for (int r = 0; r < 4; ++r) a[r] = keep[j][r];
+            } else read_cat(opp(st, 0), j, a);
+            if (KB == 0) gather_cat(tcp(st, 2), code1, j, b);
+            else if (KB == 1) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) b[r] = keep[j][r];
-          } else read_cat(opp(st, 0), j, b);
+              for (int r = 0; r < 4; ++r) b[r] = keep[j][r];
+            } else read_cat(opp(st, 0), j, b);
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            x[j][r] = a[r] * b[r];
-            hm = max(hm, __double2hiint(x[j][r]));
+            for (int r = 0; r < 4; ++r) {
+              x[j][r] = a[r] * b[r];
+              hm = max(hm, __double2hiint(x[j][r]));
+            }
+          }
+        };
+        if constexpr (LCV >= 4) {
+          // one lane per pattern: a single copy with the operand tests inside
+          // (specialising costs C3 ~1 %)
+#pragma unroll
+          for (int j = 0; j < LCV; ++j) {
+            double a[4], b[4];
+            if (d.y <= N) gather_cat(tcp(st, 1), code0, j, a);
+            else if (d.y == last) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) a[r] = keep[j][r];
+            } else read_cat(opp(st, 0), j, a);
+            if (d.z <= N) gather_cat(tcp(st, 2), code1, j, b);
+            else if (d.z == last) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) b[r] = keep[j][r];
+            } else read_cat(opp(st, 0), j, b);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              x[j][r] = a[r] * b[r];
+              hm = max(hm, __double2hiint(x[j][r]));
+            }
+          }
+        } else {
+          const int ka = d.y <= N ? 0 : d.y == last ? 1 : 2;
+          const int kb = d.z <= N ? 0 : d.z == last ? 1 : 2;
+          using K0 = std::integral_constant<int, 0>;
+          using K1 = std::integral_constant<int, 1>;
+          using K2 = std::integral_constant<int, 2>;
+          if (ka == 0) {
+            if (kb == 0) cat_loop(K0{}, K0{});
+            else cat_loop(K0{}, K1{});
+          } else if (ka == 1) {
+            if (kb == 0) cat_loop(K1{}, K0{});
+            else cat_loop(K1{}, K2{});
+          } else {
+            cat_loop(K2{}, K1{});
           }
         }
         if (!p.disable) {
