@@ -139,6 +139,10 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
                     bool(rev.value), cr, cp, codes, w, bool(spec.clock))
 
 
+def tips_of(cfg) -> int:
+    return int(cfg["tips"])
+
+
 def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: int = 12146,
                     sites: int | None = None) -> Instance:
     """One rank of a node simulates the workload with every host core and
@@ -149,7 +153,15 @@ def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: i
 
     if world <= 1:
         return generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1)
-    shm = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    # node-local shared memory when it has room for the codes (N x sites
+    # bytes plus the small arrays), else /tmp
+    cfg = CONFIGS[name]
+    need = 2 * (tips_of(cfg) * (sites or cfg["sites"])) + (64 << 20)
+    shm = "/tmp"
+    if os.path.isdir("/dev/shm"):
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize > need:
+            shm = "/dev/shm"
     path = os.path.join(shm, f"pg_synth_{name}_{seed}_{sites or 0}_{tag}.npz")
     if rank == 0:
         generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1).save(path)
