@@ -357,3 +357,31 @@ def test_linear_time_scaling_exponent():
         ts.append(best)
     slope = np.polyfit(np.log(ns), np.log(ts), 1)[0]
     assert slope < 1.3, (slope, ts)
+
+
+@pytest.mark.parametrize("m,L", [(4, 1), (4, 4), (20, 4), (61, 2)])
+def test_zero_patterns(m, L):
+    """An alignment with no columns (alignment.hpp:186-229 gives no patterns):
+    logL 0 and a zero gradient / Hessian on every kernel family, like the
+    oracle (sums over an empty pattern set, engine.hpp:206-218, :267-268)."""
+    r = O.Rng(5)
+    tree_o = O.Tree.random(r, 6, 0.05, 0.5)
+    rng = np.random.default_rng(m)
+    pi = rng.dirichlet(np.ones(m))
+    q = rng.lognormal(0, 0.5, (m, m)) * pi[None, :]
+    np.fill_diagonal(q, 0)
+    np.fill_diagonal(q, -q.sum(1))
+    rates, probs = O.discrete_gamma(0.5, L) if L > 1 else ([1.0], [1.0])
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    codes = np.zeros((tree_o.tip_count, 0), np.int8)
+    ref = O.Engine(tree_o, O.Alignment.from_patterns(codes.astype(np.int32), m, np.zeros(0, np.int64), None, labels),
+                   O.Model(q, pi, False), rates, probs)
+    ll, g, h = ref.branch_gradient(True)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, tree_o.post_order)
+    eng = LikelihoodEngine(tree, SitePatternAlignment(labels, m, codes, np.zeros(0, np.int64)),
+                           SubstitutionModel(q, pi, False), RateCategories(np.asarray(rates), np.asarray(probs)))
+    rep = eng.branch_gradient(True)
+    assert ll == 0.0 and rep.log_likelihood == 0.0
+    assert np.all(rep.branch_gradient == 0.0) and np.all(g == 0.0)
+    assert np.all(rep.hessian_diagonal == 0.0) and rep.pattern_count == 0
