@@ -594,8 +594,9 @@ struct pg_engine {
     d_site_ll.ensure(size_t(std::max(P, 1)));
     d_err.ensure(3);
     d_tc.ensure(size_t(B()) * L * NC * MP);
+    // Q P column tables: tip Q e in walkm, and in walk4's pre-order pass
+    if (use_walkm || use_walk4) d_qtc.ensure(size_t(B()) * L * NC * MP);
     if (use_walkm) {
-      d_qtc.ensure(size_t(B()) * L * NC * MP);
       const size_t frag = size_t(MP / 4) * ((MP / 4 + 1) / 2) * 32;  // WalkMGeom<MP>::FRAG
       d_fpp.ensure(size_t(B()) * L * frag);
       d_fpt.ensure(size_t(B()) * L * frag);
@@ -789,7 +790,7 @@ void pg_engine::launch_tc() {
   p.eig_w = d_ew.p;
   p.amb = d_amb.p;
   p.tc = d_tc.p;
-  p.qtc = use_walkm ? d_qtc.p : nullptr;
+  p.qtc = (use_walkm || use_walk4) ? d_qtc.p : nullptr;
   p.fpp = use_walkm ? d_fpp.p : nullptr;
   p.fpt = use_walkm ? d_fpt.p : nullptr;
   p.err = d_err.p;
@@ -812,7 +813,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   p.codes = d_codes.p;
   p.weights = d_weights.p;
   p.tc = d_tc.p;
-  p.qtc = use_walkm ? d_qtc.p : nullptr;
+  p.qtc = (use_walkm || use_walk4) ? d_qtc.p : nullptr;
   p.qtab = d_qtab.p;
   p.qidx = d_qidx.p;
   p.pi = d_pi.p;

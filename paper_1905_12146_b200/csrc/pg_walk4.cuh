@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   constexpr int VEC = 32 * LCV * MP;         // doubles per node slot of one warp
   constexpr int SD2 = VEC / 2;               // double2 per node slot
   constexpr int STAGE = 3 * SD2 + 3 * TCC + 4;  // double2 per stage: 3 operand slots, 3 TC blocks, 2x32 B codes
+  static_assert(TCC <= SD2, "a TC block fits in an operand slot");
   const WalkParams& p = P4.p;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -138,6 +139,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   };
   auto code_of = [&](int stage, int which) -> int {
     return reinterpret_cast<const uint8_t*>(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2)[pl];
+  };
+  // a tip child's Q P column table (same layout as its TC block) goes into the
+  // operand slot a tip does not use (pre-order pass), replacing the 16-FMA
+  // Q e per category: one lane per pattern only (C3 153.9 -> 151.9 ms; with
+  // two lanes per pattern it costs C2 1.33 -> 1.39 ms)
+  const bool tipq = LCV >= 4 && p.qtc != nullptr;
+  auto stage_qtc = [&](int stage, int slot, int node) {
+    const double2* gs = reinterpret_cast<const double2*>(p.qtc) + size_t(node - 1) * TCC;
+    double2* d = wsm + stage * STAGE + slot * SD2;
+#pragma unroll
+    for (int c = 0; c < (TCC + 31) / 32; ++c)
+      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
+  };
+  auto qtp = [&](int stage, int slot) -> const double* {
+    return reinterpret_cast<const double*>(wsm + stage * STAGE + slot * SD2);
   };
   auto stage_tc = [&](int stage, int slot, int node) {
     const double2* gs = reinterpret_cast<const double2*>(p.tc) + size_t(node - 1) * TCC;
@@ -368,10 +384,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
       auto issue = [&](int j, const int4 d, int prev_next) {
         const int st = j & 1;
         if (d.x != root && prev_next != d.x) stage_slot(st, 2, Qw + size_t(d.x) * SD2);
-        if (d.y <= N) stage_codes(st, 0, codes + size_t(d.y - 1) * P);
-        else stage_slot_once(st, 0, Eb + size_t(d.y) * SD2);
-        if (d.z <= N) stage_codes(st, 1, codes + size_t(d.z - 1) * P);
-        else stage_slot_once(st, 1, Eb + size_t(d.z) * SD2);
+        if (d.y <= N) {
+          stage_codes(st, 0, codes + size_t(d.y - 1) * P);
+          if (tipq) stage_qtc(st, 0, d.y);
+        } else {
+          stage_slot_once(st, 0, Eb + size_t(d.y) * SD2);
+        }
+        if (d.z <= N) {
+          stage_codes(st, 1, codes + size_t(d.z - 1) * P);
+          if (tipq) stage_qtc(st, 1, d.z);
+        } else {
+          stage_slot_once(st, 1, Eb + size_t(d.z) * SD2);
+        }
         stage_tc(st, 0, d.y);
         stage_tc(st, 1, d.z);
       };
@@ -445,17 +469,44 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
             }
             den = fma(cw[j], dd, den);
             // gradient numerators: top . (Q e), Hessian: top . (Q^2 e)
+            // Q e: a mat-vec for an internal child; for a tip the column of
+            // the staged Q P table (P and Q commute, engine.hpp:260)
             double qea[4], qeb[4];
+            if constexpr (LCV < 4) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              double u = 0.0, v = 0.0;
+              for (int r = 0; r < 4; ++r) {
+                double u = 0.0, v = 0.0;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                u = fma(qm(d.y, r, c), ea[c], u);
-                v = fma(qm(d.z, r, c), eb[c], v);
+                for (int c = 0; c < 4; ++c) {
+                  u = fma(qm(d.y, r, c), ea[c], u);
+                  v = fma(qm(d.z, r, c), eb[c], v);
+                }
+                qea[r] = u;
+                qeb[r] = v;
               }
-              qea[r] = u;
-              qeb[r] = v;
+            } else {
+              if (AI || !tipq) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  double u = 0.0;
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) u = fma(qm(d.y, r, c), ea[c], u);
+                  qea[r] = u;
+                }
+              } else {
+                gather_cat(qtp(st, 0), code0, j, qea);
+              }
+              if (BI || !tipq) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  double v = 0.0;
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) v = fma(qm(d.z, r, c), eb[c], v);
+                  qeb[r] = v;
+                }
+              } else {
+                gather_cat(qtp(st, 1), code1, j, qeb);
+              }
             }
             double d1a = 0.0, d1b = 0.0;
 #pragma unroll
