@@ -14,9 +14,17 @@
 // odd number of k-steps (20 states: K = 5) the last D entry is padding and
 // is dropped.
 //
+// Staging (MP <= 32): scratch is CTA-major, so each operand of the lock-step
+// CTA — an internal child's edge-message slots, the parent's pre-partial
+// slots, or a tip child's whole column table — is one 1-D bulk copy into
+// shared memory, issued while the previous unit computes; a tip's Q P table
+// goes into the P^T buffer the tip does not need.  MP = 64 (codons) has no
+// room for staged operands next to its 32 KB matrix blocks and loads them
+// at use.
+//
 // Scaling: categories are processed one at a time, so each (pattern,
-// category) vector carries its own power-of-two exponent (stored beside the
-// scratch slots); mixtures over categories (root likelihood, gradient
+// category) vector carries its own power-of-two exponent (stored in the tail
+// of its scratch slot); mixtures over categories (root likelihood, gradient
 // numerator/denominator) are combined with those exponents.  Post partials are
 // normalised per category at every node (exact), pre partials when produced.
 #pragma once
@@ -300,9 +308,9 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       for (int kp = 0; kp < K / 2; ++kp) __stcg(dst + kp * 32, make_double2(v[2 * kp], v[2 * kp + 1]));
       if constexpr (K & 1) __stcg(reinterpret_cast<double*>(dst - lane + (K / 2) * 32) + lane, v[K - 1]);
     };
-    // ---- staged operands (SOP): the next unit's operands are copied into a
-    // per-warp shared stage (bulk copies for scratch slots, per-lane cp.async
-    // gathers for tip columns) while this unit computes
+    // ---- staged operands (SOP): the next unit's operands are copied into the
+    // CTA's shared stage (bulk copies of slots and tip column tables; per-lane
+    // cp.async gathers when a table does not fit) while this unit computes
     auto opbuf = [&](int stage, int which) -> double* { return sop_cta + ((stage * 3 + which) * WPC + wib) * SL; };
     auto xpbuf = [&](int stage, int which) -> int* { return reinterpret_cast<int*>(opbuf(stage, which) + K * 32); };
     // the CTA's slots of one operand (WPC x (K x 32 doubles + 8 exponents)):
