@@ -437,6 +437,12 @@ def main():
         roof.update({"kernel": eng.info()["kernel"] + " (post + pre + fused gradient)", "walk_ms": walk_ms_max,
                      "traffic": prof["dram_bytes_per_launch"] if prof else None,
                      "traffic_source": prof.get("source") if prof else None})
+        if prof:
+            # pipe utilisation of the same ncu capture (DMMA sub-pipe for the
+            # tensor-bound kernels, fp64 FMA pipe and DRAM throughput otherwise)
+            for k in ("dmma_pipe_active_pct", "fp64_pipe_active_pct", "dram_throughput_pct_of_peak"):
+                if k in prof:
+                    roof["ncu_" + k] = prof[k]
         value = P_total * B / (ms * 1e-3)
         info = eng.info()
         line = {
