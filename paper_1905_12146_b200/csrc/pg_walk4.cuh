@@ -22,6 +22,12 @@
 
 #include "pg_walk.cuh"
 
+// 1: the pre-partial of the child visited next is held in registers
+// (qreg) instead of the next stage's shared q slot
+#ifndef PG_WALK4_QREG
+#define PG_WALK4_QREG 0
+#endif
+
 namespace pgk {
 
 __device__ __forceinline__ void cp16_cg(void* smem, const void* gmem) {
@@ -399,12 +405,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
         stage_tc(st, 0, d.y);
         stage_tc(st, 1, d.z);
       };
+#if PG_WALK4_QREG
       double qreg[LCV][4];
+#endif
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
       int4 dnext = shfl4(win, 0);
       issue(0, dnext, 0);
       cp_commit();
+#if !PG_WALK4_QREG
+      // the pre-partial operand always comes from the stage's q slot: the
+      // root's is pi, written here (the first step is the root's)
+#pragma unroll
+      for (int j = 0; j < LCV; ++j) {
+        double2* qd = opp(0, 2);
+        qd[(2 * j) * 32] = make_double2(P4.pi[0], P4.pi[1]);
+        qd[(2 * j + 1) * 32] = make_double2(P4.pi[2], P4.pi[3]);
+      }
+#endif
       int prev_next = 0;
       for (int i = 0; i < n; ++i) {
         const int4 d = dnext;
@@ -447,6 +465,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
 #pragma unroll
           for (int j = 0; j < LCV; ++j) {
             double q[4], ea[4], eb[4];
+#if PG_WALK4_QREG
             if (d.x == root) {
 #pragma unroll
               for (int r = 0; r < 4; ++r) q[r] = P4.pi[r];
@@ -456,6 +475,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
             } else {
               read_cat(opp(st, 2), j, q);
             }
+#else
+            read_cat(opp(st, 2), j, q);
+#endif
             if (AI) read_cat(opp(st, 0), j, ea);
             else gather_cat(Ta, code0, j, ea);
             if (BI) read_cat(opp(st, 1), j, eb);
@@ -592,15 +614,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
           }
         }
         // normalise and hand on the pre-partials of internal children: the one
-        // visited next stays in registers, the other goes to its scratch slot
+        // visited next goes straight into the next stage's q slot (not staged
+        // from memory for that step), the other to its scratch slot
         auto emit = [&](const int x, double(&qx)[LCV][4], const int hx) {
           const int ex = peak_exponent(hx);
           const double scl = (ex != 0 && ex <= 1022) ? pow2_neg(ex) : 1.0;
           if (x == d.w) {
+#if PG_WALK4_QREG
 #pragma unroll
             for (int j = 0; j < LCV; ++j)
 #pragma unroll
               for (int r = 0; r < 4; ++r) qreg[j][r] = qx[j][r] * scl;
+#else
+            double2* qd = opp(st ^ 1, 2);
+#pragma unroll
+            for (int j = 0; j < LCV; ++j) {
+              qd[(2 * j) * 32] = make_double2(qx[j][0] * scl, qx[j][1] * scl);
+              qd[(2 * j + 1) * 32] = make_double2(qx[j][2] * scl, qx[j][3] * scl);
+            }
+#endif
           } else {
             double2* dst = Qw + size_t(x) * SD2;
 #pragma unroll
