@@ -225,9 +225,11 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
   // homogeneous Q staged in smem; per-branch generators read in fragment order from global
   const bool homog = PM.homogeneous != 0;
-  auto matvec_Q = [&](const double* Qf, const double (&x)[K], double (&y)[K]) {
+  // y = Q_x x for the generator of node x's branch (shared generator staged
+  // in shared memory; per-branch ones in fragment order from global)
+  auto matvec_Q = [&](int x_node, const double (&x)[K], double (&y)[K]) {
     if (homog) matvec(Qsm, x, y);
-    else matvec_g(Qf, x, y);
+    else matvec_g(PM.fq + size_t(p.qidx[x_node]) * FRAG, x, y);
   };
   auto quad_sum = [&](double v) {
     v += __shfl_xor_sync(kFull, v, 1);
@@ -593,8 +595,6 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         } else {
           load_pre(stc, cc0, cc1, l, qv, ea, eb, xq, xa, xb);
         }
-        const double* Qa = PM.fq + size_t(homog ? 0 : p.qidx[ca]) * FRAG;
-        const double* Qb = PM.fq + size_t(homog ? 0 : p.qidx[cb]) * FRAG;
         const int El = xq + xa + xb;
         double ta[K], tb[K], dd = 0.0;
 #pragma unroll
@@ -608,10 +608,10 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         term[0] = wl * quad_sum(dd);
         {
           double ua[K], ub[K];
-          if (a_int) matvec_Q(Qa, ea, ua);
+          if (a_int) matvec_Q(ca, ea, ua);
           else if (qstage) staged_q(pbuf(0, par), cc0, ua);
           else gather_q(ca, cc0, l, ua);
-          if (b_int) matvec_Q(Qb, eb, ub);
+          if (b_int) matvec_Q(cb, eb, ub);
           else if (qstage) staged_q(pbuf(1, par), cc1, ub);
           else gather_q(cb, cc1, l, ub);
           double d1a = 0.0, d1b = 0.0;
@@ -624,8 +624,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           term[2] = cl * wl * quad_sum(d1b);
           if constexpr (HESS) {
             double u2a[K], u2b[K];
-            matvec_Q(Qa, ua, u2a);
-            matvec_Q(Qb, ub, u2b);
+            matvec_Q(ca, ua, u2a);
+            matvec_Q(cb, ub, u2b);
             double d2a = 0.0, d2b = 0.0;
 #pragma unroll
             for (int ki = 0; ki < K; ++ki) {
