@@ -109,7 +109,11 @@ struct WalkMGeom {
   static constexpr int SOPD = SOP ? 6 * SL : 0;
   // P(t) blocks (two children of a pre-order step, x2 parities if PIPE) + Q
   // + SOP + two mbarriers (one per buffer parity) for the bulk copies
-  static constexpr size_t smem_bytes() { return size_t((NPB + 1) * FRAG + WPC * SOPD + 2) * sizeof(double); }
+  // + two mbarriers, pi (MP) and up to kSmemCats category weights and rates
+  static constexpr int kSmemCats = 16;
+  static constexpr size_t smem_bytes() {
+    return size_t((NPB + 1) * FRAG + WPC * SOPD + 2 + MP + 2 * kSmemCats) * sizeof(double);
+  }
 };
 
 // HESS: Hessian-diagonal variant (a template parameter so the gradient-only
@@ -270,10 +274,20 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     int ref;
   };
 
-  if (homog) {
+  // pi and the category weights / rates in shared memory (read every unit)
+  double* pism = reinterpret_cast<double*>(mbar + 2);
+  double* probsm = pism + MP;
+  double* ratesm = probsm + Gm::kSmemCats;
+  const bool cats_sm = p.L <= Gm::kSmemCats;
+  for (int i = tid; i < MP; i += CT) pism[i] = p.pi[i];
+  if (cats_sm)
+    for (int i = tid; i < p.L; i += CT) {
+      probsm[i] = p.probs[i];
+      ratesm[i] = p.rates[i];
+    }
+  if (homog)
     for (int i = tid; i < FRAG; i += CT) Qsm[i] = PM.fq[i];
-    __syncthreads();
-  }
+  __syncthreads();
 
   for (int tile = blockIdx.x; tile < ntile_cta; tile += gridDim.x) {
     const int s = tile * (8 * WPC) + wib * 8 + q;
@@ -450,8 +464,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (stc.x == root) {
           double d = 0.0;
 #pragma unroll
-          for (int ki = 0; ki < K; ++ki) d = fma(p.pi[ki * 4 + t], a[ki], d);
-          d = quad_sum(d) * p.probs[l];
+          for (int ki = 0; ki < K; ++ki) d = fma(pism[ki * 4 + t], a[ki], d);
+          d = quad_sum(d) * (cats_sm ? probsm[l] : p.probs[l]);
           if (Sk > mix.ref) {
             mix.v[0] = mix.ref == INT_MIN ? 0.0 : mix.v[0] * pow2(mix.ref - Sk);
             mix.ref = Sk;
@@ -500,7 +514,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         xq = xa = xb = 0;
         if (st.x == root) {
 #pragma unroll
-          for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
+          for (int ki = 0; ki < K; ++ki) qv[ki] = pism[ki * 4 + t];
         } else {
           load_slot(Qs, st.x, l, qv);
           xq = *xslot(Qs, st.x, l);
@@ -584,7 +598,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         if (sop) {
           if (stc.x == root) {
 #pragma unroll
-            for (int ki = 0; ki < K; ++ki) qv[ki] = p.pi[ki * 4 + t];
+            for (int ki = 0; ki < K; ++ki) qv[ki] = pism[ki * 4 + t];
           } else {
             read_op(u & 1, 2, qv, xq);
           }
@@ -603,7 +617,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
           tb[ki] = qv[ki] * ea[ki];
           dd = fma(ta[ki], ea[ki], dd);
         }
-        const double wl = p.probs[l], cl = p.rates[l];
+        const double wl = cats_sm ? probsm[l] : p.probs[l], cl = cats_sm ? ratesm[l] : p.rates[l];
         double term[NR];
         term[0] = wl * quad_sum(dd);
         {
