@@ -24,3 +24,34 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_device_arm_json_line():
+    """The device arm on a small C2 sample: one JSON line with the keys the
+    driver reads (value, e2e with copied bytes, roofline with the kernel's
+    algorithmic bytes, cpu_baseline with its one-thread variant, launches,
+    clocks)."""
+    out = subprocess.run([sys.executable, "bench.py", "--config", "C2", "--sites", "3000", "--steps", "3",
+                          "--warmup", "3", "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["metric"] == "pattern x branch gradient updates/s (full logL + grad eval)"
+    assert d["unit"] == "pattern-branch/s" and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["dtype"] == "f64"
+    assert d["config"]["workload"] == "C2"
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12 and r["algorithmic_bytes_per_launch"] > 0
+    assert d["gpu_launches"] == 3 * 3  # K1, walk, K3 per evaluation
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["value"] > 0 and cb["single_thread"]["cores"] == 1
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
