@@ -5,22 +5,31 @@ full logL + branch(-rate) gradient evaluation (BASELINE.json metric).
 One step = one full evaluation of the hot path over the whole synthetic
 workload: P(t) build (K1), post-order + pre-order walk with the fused gradient
 (K2), fixed-order reduction with the clock chain rule (K3), and for N > 1 the
-NCCL all-reduce of [logL, grad].  Patterns are sharded contiguously over ranks
-(weak in the per-GPU sense: each rank owns P/N patterns of the same job; the
-job itself is fixed, so scaling is reported as "strong").
+NCCL all-reduce of [logL, grad].  The job (all patterns of the config) is
+fixed; N ranks each own a contiguous block of it (scaling "strong").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+--gpus N > 1 outside torchrun re-launches itself under
+torch.distributed.run with N processes (one per GPU, 127.0.0.1 rendezvous).
 
 Default workload: C3 (BASELINE.json configs[2]): 2048-taxon Yule tree,
 general non-reversible 4-state Q + Gamma4, 1,000,000 simulated columns,
 gradient w.r.t. 4,094 branch-specific clock rates — the largest config and the
 one BASELINE.json quotes "1/2/4/8 GPUs" on.  --impl reference times the CPU
 restatement of the reference engine (oracle/, "port": the reference itself needs
-Eigen + Boost, absent here) on the host cores on a bounded pattern sample.
+Eigen + Boost, absent here) on the host cores on a bounded pattern sample; its
+inputs come from workloads/ (a host library separate from the product), so the
+reference arm never maps libphylograd_b200.so.
+
+At full size the device arm checks its result against the committed
+full-size oracle fixture (tests/golden/full_<config>.npz, made by
+tests/golden/make_fullsize.py) and reports it as "parity".
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,9 +42,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 12146
+METRIC = "pattern x branch gradient updates/s (full logL + grad eval)"
+UNIT = "pattern-branch/s"
+L2_NOTE = "inputs larger than L2 (edge scratch + tip codes >> 126 MB); no flush"
+PARALLELISM = "contiguous pattern blocks (GPU: one rank per GPU + NCCL all-reduce; CPU: std::thread blocks)"
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -46,8 +59,9 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=None, help="patterns in the CPU baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work timed for the cpu_baseline (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size fixture check")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period in the timed region (0: off)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -57,16 +71,46 @@ def dist_env():
     return rank, world, local
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_command(args, argv):
+    """--gpus N > 1 outside torchrun: the same command under
+    torch.distributed.run, one process per GPU (None: run in this process)."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1 or args.impl == "reference":
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + list(argv)
+
+
+# ------------------------------------------------------------ work models
 def bytes_alg(inst, patterns):
-    """B_alg = 40 L m (N-2) P + 2 N P (5 fp64 m-vectors per
-    internal non-root node per pattern-category + uint8 tip codes per pass)."""
+    """Algorithmic DRAM bytes of one evaluation: every
+    internal non-root node's edge message e = P p (L m doubles per pattern) is
+    written once by the post-order pass and read once by the pre-order pass —
+    the pre-order step of a node needs both children's e, and no e survives on
+    chip across the whole post pass — plus the uint8 tip codes read once per
+    pass: 16 L m (N-2) P + 2 N P.  (The pre-partial of the child visited next
+    stays on chip; the deferred one is re-read from L2.)"""
     L = len(inst.cat_rates)
-    m = inst.states
-    N = inst.tip_count
-    return 40.0 * L * m * (N - 2) * patterns + 2.0 * N * patterns
+    return 16.0 * L * inst.states * (inst.tip_count - 2) * patterns + 2.0 * inst.tip_count * patterns
+
+
+def bytes_survey(inst, patterns):
+    """SURVEY.md §8d canonical B_alg = 40 L m (N-2) P + 2 N P (5 materialised
+    m-vectors per internal node-category): kept for comparison only."""
+    L = len(inst.cat_rates)
+    return 40.0 * L * inst.states * (inst.tip_count - 2) * patterns + 2.0 * inst.tip_count * patterns
 
 
 def flops_alg(inst, patterns):
+    """SURVEY.md §8d F_alg = 6 m^2 (N-2) L P: three dense m x m mat-vecs per
+    internal non-root node per pattern-category."""
     L = len(inst.cat_rates)
     return 6.0 * inst.states ** 2 * (inst.tip_count - 2) * L * patterns
 
@@ -75,7 +119,7 @@ def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return 6650.0, "fallback"
 
@@ -88,23 +132,65 @@ def fp64_tensor_peak():
             for line in f:
                 d = json.loads(line)
                 if d.get("kernel", "").startswith("dmma"):
-                    return float(d["tflops"]), "measured (scripts/fp64_peak.cu)"
+                    return float(d["tflops"]), "measured (scripts/fp64_peak.cu, profiles/fp64_peak_b200.json)"
     except Exception:
         pass
     return 37.0, "fallback (datasheet)"
 
 
-def profiled_traffic(config):
-    """DRAM bytes per walk launch from the committed ncu capture, if any."""
+def profiled_traffic(config, patterns, world):
+    """DRAM bytes per walk launch from the committed full-size ncu capture of
+    this config — only when this run is that workload (same pattern count,
+    one GPU); otherwise None."""
+    if world != 1:
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_walk_summary.json")) as f:
-            d = json.load(f)
-        rec = d.get(config)
-        if rec:
+            rec = json.load(f).get(config)
+        if rec and int(rec.get("patterns", -1)) == int(patterns):
             return rec
     except Exception:
         pass
     return None
+
+
+def roofline_block(inst, patterns, walk_ms, kernel, world, config):
+    """Roofline of the dominant kernel (the walk).  The bound follows the
+    arithmetic intensity F_alg / B_alg against the ridge of the measured
+    peaks (fp64 DMMA / HBM): 4-state models are HBM-bound (1.5 flop/B), the
+    20- and 61-state ones fp64-tensor-bound (7.5 and 22.9 flop/B vs a ridge
+    of ~5.7)."""
+    hbm, hbm_src = measured_peaks()
+    tf, tf_src = fp64_tensor_peak()
+    balg, falg = bytes_alg(inst, patterns), flops_alg(inst, patterns)
+    t = walk_ms * 1e-3
+    ridge = tf * 1e12 / (hbm * 1e9)
+    prof = profiled_traffic(config, inst.patterns, world)
+    if falg / balg > ridge:
+        achieved = falg / t / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s", "frac": achieved / tf,
+                "peak_source": tf_src}
+    else:
+        achieved = balg / t / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": hbm_src}
+    roof.update({
+        "traffic": prof["dram_bytes_per_launch"] if prof else None,
+        "kernel": kernel + " (post + pre + fused gradient)", "walk_ms": walk_ms,
+        "algorithmic_bytes_per_launch": balg, "algorithmic_flops_per_launch": falg,
+        "bytes_model": "16 L m (N-2) P + 2 N P (edge message of each internal non-root node written once, read once)",
+        "arithmetic_intensity": falg / balg, "ridge_flop_per_byte": ridge,
+        "survey_b_alg_bytes": bytes_survey(inst, patterns),
+        "survey_b_alg_frac_of_hbm": bytes_survey(inst, patterns) / t / 1e9 / hbm,
+    })
+    if prof:
+        dram = prof["dram_bytes_per_launch"] / t / 1e9
+        roof.update({"traffic_source": prof.get("source"), "dram_achieved_gbps": dram, "dram_frac_of_hbm": dram / hbm,
+                     "traffic_over_algorithmic": prof["dram_bytes_per_launch"] / balg})
+        for k in ("dmma_pipe_active_pct", "fp64_pipe_active_pct", "dram_throughput_pct_of_peak"):
+            if k in prof:
+                roof["ncu_" + k] = prof[k]
+    return roof
 
 
 class ClockSampler:
@@ -245,11 +331,46 @@ def default_sample(inst):
     return int(max(32, min(inst.patterns, 6.0e9 / per_pattern)))
 
 
+def bench_config(args, inst):
+    """The workload description, identical in both arms (same keys, same
+    values), so the driver's same-config check compares like with like."""
+    from workloads import synth
+
+    return {"workload": args.config, "description": synth.DESCRIPTIONS[args.config], "seed": SEED,
+            "sites": int(inst.weights.sum()), "patterns": inst.patterns, "branches": inst.branches,
+            "tips": inst.tip_count, "states": inst.states, "categories": len(inst.cat_rates),
+            "gradient": "branch rates (dt*g)" if inst.clock else "branch lengths", "parallelism": PARALLELISM,
+            "l2": L2_NOTE}
+
+
+def parity_block(args, inst, logl, grad):
+    """The device result against the full-size oracle fixture of this exact
+    workload (tests/golden/full_<config>.npz; instance digest must match)."""
+    from workloads import synth
+
+    path = os.path.join(ROOT, "tests", "golden", f"full_{args.config}.npz")
+    rel = os.path.relpath(path, ROOT)
+    if args.sites is not None or not os.path.exists(path):
+        return {"fixture": None, "note": "no full-size fixture for this workload"}
+    fx = np.load(path)
+    if synth.instance_digest(inst) != str(fx["digest"]):
+        return {"fixture": rel, "match": False, "note": "instance digest differs from the fixture's"}
+    want = fx["rate_gradient"] if inst.clock else fx["gradient"]
+    g = np.asarray(grad)
+    err = np.abs(g - want)
+    scale = float(np.max(np.abs(want)))
+    ok = bool(np.all(np.isfinite(g)) and np.all(err <= 1e-9 * np.abs(want) + 1e-12 * scale))
+    ll_rel = abs(logl - float(fx["logL"])) / abs(float(fx["logL"]))
+    return {"fixture": rel, "match": True, "logL_rel": ll_rel,
+            "grad_max_rel": float(np.max(err / np.maximum(np.abs(want), 1e-300))),
+            "grad_max_rel_to_scale": float(np.max(err) / scale),
+            "within_1e-9": bool(ok and ll_rel <= 1e-9), "oracle_threads": int(fx["oracle_threads"])}
+
+
 def run_reference(args, inst):
     threads = os.cpu_count() or 1
     sample = args.cpu_sample or default_sample(inst)
     B = inst.branches
-    rates = []
     from tests.helpers import oracle_for
 
     sub = inst.slice_patterns(0, min(sample, inst.patterns))
@@ -283,34 +404,24 @@ def run_reference(args, inst):
         how += (f", extrapolated to all {inst.patterns} ({fixed * 1e3:.1f} ms fixed + "
                 f"{slope * 1e6:.3f} us/pattern, fixed part from a {sub.patterns // 4}-pattern sample)")
     line = {
-        "impl": "reference", "metric": "pattern x branch gradient updates/s (full logL + grad eval)",
-        "value": value, "unit": "pattern-branch/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded; BASELINE.json config)",
-        "config": {"workload": args.config, "sample_patterns": sub.patterns, "full_patterns": inst.patterns,
-                   "branches": B, "tips": inst.tip_count, "states": inst.states,
-                   "categories": len(inst.cat_rates)},
-        "cpu_baseline": {"value": value, "unit": "pattern-branch/s", "cores": threads, "kind": "port",
+        "dtype": "f64", "data": "synthetic (seeded; BASELINE.json config shapes)",
+        "config": bench_config(args, inst),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{how}, full tree, {threads} pattern blocks on std::threads; {cpu_model()}"},
-        "e2e": {"value": value, "unit": "pattern-branch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse_args()
-    rank, world, local = dist_env()
-    from paper_1905_12146_b200 import synth
-
-    if args.impl == "reference":
-        if rank != 0:
-            return 0
-        inst = synth.generate(args.config, seed=SEED, sites=args.sites)
-        run_reference(args, inst)
-        return 0
-
+def run_device(args):
     import torch
 
+    from workloads import synth
+
+    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -321,12 +432,21 @@ def main():
                                  tag=str(os.getppid()), seed=SEED, sites=args.sites)
     t_gen = time.perf_counter() - t_gen
     P_total = inst.patterns
-    p0, p1 = P_total * rank // world, P_total * (rank + 1) // world
-    shard = inst.slice_patterns(p0, p1)
     from paper_1905_12146_b200 import _lib as _L
     from paper_1905_12146_b200.api import EngineOptions
 
-    eng = synth.engine_for(shard, EngineOptions(device=local))
+    opts = EngineOptions(device=local)
+    if world > 1:
+        # the product's ShardedEngine: this rank's contiguous block + one
+        # NCCL all-reduce of [logL, g] per evaluation on the engine stream
+        from paper_1905_12146_b200.sharding import ShardedEngine
+
+        sh = ShardedEngine(*synth.api_objects(inst), opts)
+        if inst.clock:
+            sh.set_clock_durations(inst.durations)
+        eng, p0, p1 = sh.local, sh.p0, sh.p1
+    else:
+        sh, eng, p0, p1 = None, synth.engine_for(inst, opts), 0, P_total
     L = _L.lib()
     B = inst.branches
     stream = torch.cuda.current_stream()
@@ -335,9 +455,10 @@ def main():
     out = torch.zeros(1 + B, dtype=torch.float64, device="cuda")
 
     def step_device():
-        _L.check(L.pg_evaluate_device(eng.handle, flags, out.data_ptr()))
-        if world > 1:
-            torch.distributed.all_reduce(out)
+        if sh is not None:
+            sh.enqueue_device(flags, out)
+        else:
+            _L.check(L.pg_evaluate_device(eng.handle, flags, out.data_ptr()))
 
     for _ in range(args.warmup):
         step_device()
@@ -361,6 +482,8 @@ def main():
             step_device()
         ev1.record(stream)
         barrier()
+    # the device error flags are sticky until read: this reports a non-finite
+    # or underflowed site in ANY of the timed evaluations
     _L.check(L.pg_check_errors(eng.handle))
     ms = ev0.elapsed_time(ev1) / args.steps
     n_ev, walk_tot, eval_tot = C.c_int(), C.c_double(), C.c_double()
@@ -370,34 +493,21 @@ def main():
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms, walk_ms_max = float(t[0]), float(t[1])
-    logl = float(out[0])
+    res = out.cpu().numpy()
+    logl = float(res[0])
 
     # ---- end-to-end through the public API with host buffers (e2e)
-    b_host = [torch.from_numpy(inst.branch_rates if inst.clock else inst.branch_lengths).double().pin_memory()]
-    b_host.append((b_host[0] * (1.0 + 1e-12)).pin_memory())
-    res_host = torch.empty(1 + B, dtype=torch.float64).pin_memory()
-    b_dev = torch.empty(B, dtype=torch.float64, device="cuda")
-    dt_dev = torch.from_numpy(inst.durations).cuda() if inst.clock else None
-
     b_np = [inst.branch_rates if inst.clock else inst.branch_lengths]
     b_np.append(b_np[0] * (1.0 + 1e-12))
 
     def step_e2e(i):
-        if world == 1:
-            # the user-facing call: host vector in, GradientReport (host) out
-            b = b_np[i % 2] * inst.durations if inst.clock else b_np[i % 2]   # b_i = r_i dt_i (clock.hpp:42-55)
-            eng.set_branch_lengths(b)
-            rep = eng.rate_gradient() if inst.clock else eng.branch_gradient()
-            return rep.log_likelihood
-        b_dev.copy_(b_host[i % 2], non_blocking=True)  # H2D of this step's rates / lengths
-        bl = b_dev * dt_dev if inst.clock else b_dev
-        _L.check(L.pg_set_branch_lengths_device(eng.handle, bl.data_ptr()))
-        _L.check(L.pg_evaluate_device(eng.handle, flags, out.data_ptr()))
-        torch.distributed.all_reduce(out)
-        res_host.copy_(out, non_blocking=True)             # D2H of [logL, grad]
-        torch.cuda.current_stream().synchronize()
-        _L.check(L.pg_check_errors(eng.handle))
-        return float(res_host[0])
+        # the user-facing call: host vector in (H2D inside set_branch_lengths),
+        # GradientReport on the host out (D2H of [logL, g])
+        b = b_np[i % 2] * inst.durations if inst.clock else b_np[i % 2]   # b_i = r_i dt_i (clock.hpp:42-55)
+        target = sh if sh is not None else eng
+        target.set_branch_lengths(b)
+        rep = target.rate_gradient() if inst.clock else target.branch_gradient()
+        return rep.log_likelihood
 
     # consecutive steps alternate between two distinct vectors so no step can
     # hit the engine's "bit-identical lengths" cache (engine.hpp:121)
@@ -409,8 +519,7 @@ def main():
     e2e_walk = []
     for i in range(nw, nw + args.steps):
         step_e2e(i)
-        if world == 1:
-            e2e_walk.append(round(eng.last_times_ms()[0], 2))
+        e2e_walk.append(round(eng.last_times_ms()[0], 2))
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
     print(f"e2e walk ms per step: {e2e_walk}", file=sys.stderr)
@@ -420,55 +529,33 @@ def main():
     e2e_s = float(te[0])
 
     if rank == 0:
-        prof = profiled_traffic(args.config)
-        if inst.states > 32:
-            # codon path: fp64 tensor-core bound (AI = 9.2 flop/B)
-            peak, peak_kind = fp64_tensor_peak()
-            falg = flops_alg(inst, p1 - p0)
-            achieved = falg / (walk_ms_max * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "peak_source": peak_kind, "algorithmic_flops_per_launch": falg}
-        else:
-            peak, peak_kind = measured_peaks()
-            balg = bytes_alg(inst, p1 - p0)
-            achieved = balg / (walk_ms_max * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": balg}
-        roof.update({"kernel": eng.info()["kernel"] + " (post + pre + fused gradient)", "walk_ms": walk_ms_max,
-                     "traffic": prof["dram_bytes_per_launch"] if prof else None,
-                     "traffic_source": prof.get("source") if prof else None})
-        if prof:
-            # pipe utilisation of the same ncu capture (DMMA sub-pipe for the
-            # tensor-bound kernels, fp64 FMA pipe and DRAM throughput otherwise)
-            for k in ("dmma_pipe_active_pct", "fp64_pipe_active_pct", "dram_throughput_pct_of_peak"):
-                if k in prof:
-                    roof["ncu_" + k] = prof[k]
-        value = P_total * B / (ms * 1e-3)
         info = eng.info()
+        nccl = {"world_size": world, "comm_size": world, "version": None}
+        if world > 1:
+            nccl["comm_size"] = torch.distributed.get_world_size()
+            nccl["version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
         line = {
-            "metric": "pattern x branch gradient updates/s (full logL + grad eval)",
-            "value": value, "unit": "pattern-branch/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE.json config shapes)",
-            "config": {"workload": args.config, "description": synth.DESCRIPTIONS[args.config],
-                       "patterns": P_total, "branches": B, "tips": inst.tip_count, "states": inst.states,
-                       "categories": len(inst.cat_rates),
-                       "gradient": "branch rates (dt*g)" if inst.clock else "branch lengths",
-                       "parallelism": f"pattern-shard dp{world}",
-                       "l2": "inputs larger than L2 (edge scratch + tip codes >> 126 MB); no flush",
-                       "setup_s": round(t_gen, 2), "geometry": info},
-            "roofline": roof,
-            "e2e": {"value": P_total * B / e2e_s, "unit": "pattern-branch/s", "ms_per_step": e2e_s * 1e3,
+            "metric": METRIC, "value": P_total * B / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "world_size": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE.json config shapes)",
+            "config": bench_config(args, inst),
+            "roofline": roofline_block(inst, p1 - p0, walk_ms_max, info["kernel"], world, args.config),
+            "e2e": {"value": P_total * B / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                     "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": 8 * (1 + B)},
             "gpu_launches": info["launches"] * args.steps,
             "clocks": clocks.summary(),
             "logL": logl,
+            "parity": None if args.no_parity else parity_block(args, inst, logl, res[1:1 + B]),
+            "nccl": nccl,
+            "geometry": info, "setup_s": round(t_gen, 2), "shard_patterns": p1 - p0,
+            "errors_checked": "every timed step (sticky device error flags read after the region)",
         }
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
             sample = args.cpu_sample or default_sample(inst)
             cpu_value, how = cpu_baseline(inst, sample, threads, args.cpu_seconds)
-            line["cpu_baseline"] = {"value": cpu_value, "unit": "pattern-branch/s", "cores": threads, "kind": "port",
+            line["cpu_baseline"] = {"value": cpu_value, "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": f"full tree, invalidate+gradient: {how}; {cpu_model()}"}
             if threads > 1:
                 # SURVEY.md §8d variant (i): one thread, like the reference engine
@@ -480,6 +567,27 @@ def main():
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
+    cmd = relaunch_command(args, argv)
+    if cmd is not None:
+        return subprocess.call(cmd)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        # rank 0 alone times the CPU reference; other torchrun ranks exit
+        if rank != 0:
+            return 0
+        from workloads import synth
+
+        run_reference(args, synth.generate(args.config, seed=SEED, sites=args.sites))
+        return 0
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    return run_device(args)
 
 
 if __name__ == "__main__":

@@ -33,7 +33,8 @@ enum pg_status {
   PG_ERR_LOGIC = 3,            /* std::logic_error (pass ordering) */
   PG_ERR_NEWICK = 4,           /* phylograd::NewickError (position in pg_last_error) */
   PG_ERR_CUDA = 5,             /* device / driver failure */
-  PG_ERR_NOT_SUPPORTED = 6
+  PG_ERR_NOT_SUPPORTED = 6,
+  PG_ERR_NCCL = 7              /* NCCL load / communicator / collective failure */
 };
 
 /* Evaluation flags for pg_evaluate (engine.hpp:146-164; clock.hpp:146-152). */
@@ -69,6 +70,27 @@ const char* pg_last_error(void);
  * their host arrays after each setter returns. */
 int pg_create(const pg_options* opt, pg_engine** out);
 void pg_destroy(pg_engine* e);
+
+/* ---- multi-GPU from one process (SURVEY.md §8b pg_create(desc{G, devices}),
+ * §8e).  Patterns shard contiguously: entry r of `devices` owns patterns
+ * [floor(r P / G), floor((r+1) P / G)) and runs both traversals locally; one
+ * reduction of [logL, g (2N-2), h (2N-2)] per evaluation combines them:
+ *  - PG_REDUCE_NCCL: ncclCommInitAll over the device list (distinct devices)
+ *    and one in-place ncclAllReduce(sum, float64) per shard stream inside
+ *    ncclGroupStart/End (libnccl.so.2 is loaded at this call, not at link time);
+ *  - PG_REDUCE_FIXED_ORDER: every shard's result is copied to the first
+ *    device (peer copy) and summed in rank order 0..G-1 by one kernel, so the
+ *    result is bit-reproducible for a fixed device list; repeated devices
+ *    are allowed (several shards on one GPU).
+ * The returned handle takes every setter and pg_evaluate / pg_clock_gradient
+ * like a single-device engine (callers such as clock.hpp:146-147 and
+ * cli.hpp:313-317 need no change); device-pointer entry points, pg_set_stream
+ * and the debug partial accessors return PG_ERR_NOT_SUPPORTED on a group. */
+enum pg_reduce { PG_REDUCE_NCCL = 0, PG_REDUCE_FIXED_ORDER = 1 };
+int pg_create_multi(const pg_options* opt, int device_count, const int* devices, int reduce_mode, pg_engine** out);
+/* shard_count (1 for a single-device engine), NCCL version (0 unless the
+ * NCCL reduction is in use), reduce mode. */
+int pg_group_info(const pg_engine* e, int* shard_count, int* nccl_version, int* reduce_mode);
 
 /* tree.hpp:27-77: parent[2N] (parent[root]=0), children[2N][2] ({0,0} for
  * tips), post_order[2N-1] (validated as an admissible order: children before
@@ -106,6 +128,18 @@ int pg_get_branch_lengths(pg_engine* e, double* b);
 /* clock.hpp:42-55 / cli.hpp:429-440: calendar durations dt_i = t_i - t_pa(i)
  * used by PG_EVAL_RATE_GRAD (d logL / d r_i = dt_i g_i, b_i = r_i dt_i). */
 int pg_set_clock_durations(pg_engine* e, const double* dt);
+
+/* clock.hpp:140-152 and :199-213: the relaxed-clock chain rule from one
+ * branch-gradient evaluation at the current lengths b_i = r_i dt_i (cached
+ * like pg_evaluate(PG_EVAL_GRAD)), computed on the GPU:
+ *   dlog_eps[i] = d logL / d log eps_i = b_i g_i            (2N-2, may be NULL)
+ *   *dlog_mu    = d logL / d log mu    = sum_i b_i g_i      (fixed order, may be NULL)
+ *   dnode_time[k] = d logL / d t_{N+1+k}
+ *                 = r_{N+1+k} g_{N+1+k} [non-root] - sum_children r_c g_c  (N-1, may be NULL)
+ * rates[2N-2] are the branch rates r_i = mu eps_i (host); NULL derives them
+ * as b_i / dt_i from pg_set_clock_durations.  log_likelihood may be NULL. */
+int pg_clock_gradient(pg_engine* e, const double* rates, double* log_likelihood, double* dlog_mu, double* dlog_eps,
+                      double* dnode_time);
 
 /* engine.hpp:146-164.  Synchronous: returns when results are in host memory.
  * log_likelihood may be NULL; grad/hess (2N-2 doubles) may be NULL unless the
@@ -180,32 +214,6 @@ int pg_compress_codes_gpu(int ntax, int64_t sites, const int8_t* codes, int code
 int pg_compress_result_gpu(void* handle, int8_t* pattern_codes, int64_t* weights, int32_t* site_to_pattern,
                            float* device_ms);
 void pg_compress_free_gpu(void* handle);
-
-/* Seeded synthetic workloads standing in for the paper's datasets
- * (BASELINE.json configs): Yule tree, model draws, forward
- * simulation, optional gaps, compression.  Host-side input generation only. */
-typedef struct pg_synth_spec {
-  int tips;
-  int model_kind;        /* 0 HKY85, 1 GTR, 2 general non-reversible 4-state, 3 AA-20 reversible, 4 GY94 codon */
-  int categories;        /* 1 or discrete-gamma count */
-  double gamma_alpha;
-  int64_t sites;
-  double branch_mean;    /* Exp(mean) branch lengths (model_kind != clock) */
-  int clock;             /* 1: b_i = r_i dt_i with dt ~ Exp(dt_mean), r = rate_scale*exp(N(0, rate_sd^2)) */
-  double dt_mean, rate_scale, rate_sd;
-  double gap_fraction;   /* Bernoulli per (taxon, site) -> missing */
-  uint64_t seed;
-  int threads;           /* 0 = hardware concurrency */
-} pg_synth_spec;
-int pg_synth_create(const pg_synth_spec* spec, void** handle, int* pattern_count, int* state_count);
-/* parent[2N], children[2N*2], post_order[2N-1], branch_lengths[2N-2],
- * durations[2N-2] (zeros unless clock), rates[2N-2] (zeros unless clock). */
-int pg_synth_tree(void* handle, int32_t* parent, int32_t* children, int32_t* post_order, double* branch_lengths,
-                  double* durations, double* rates);
-int pg_synth_model(void* handle, double* q, double* pi, int* reversible, double* cat_rates, double* cat_probs);
-/* codes [tips][P] int8 (-1 missing), weights[P]. */
-int pg_synth_patterns(void* handle, int8_t* codes, int64_t* weights);
-void pg_synth_free(void* handle);
 
 /* substitution.hpp:55-68 discrete_gamma_categories (bin medians, mean one). */
 int pg_discrete_gamma(double alpha, int count, double* rates, double* probs);

@@ -15,6 +15,7 @@
 #include <array>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -35,6 +36,7 @@ inline void check(int rc) {
     case PG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case PG_ERR_LOGIC: throw std::logic_error(msg);
     case PG_ERR_NEWICK: throw NewickError(msg);
+    case PG_ERR_NOT_SUPPORTED: throw std::domain_error(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -181,6 +183,21 @@ struct EngineOptions {
   bool disable_rescaling = false;
   int device = 0;
   bool capture_partials = false;  // keep per-node partials for the engine.hpp:134-141 accessors (debug)
+  // Multi-GPU from one process (pg_create_multi): non-empty -> patterns shard
+  // contiguously over these devices, one reduction of [logL, g, h] per
+  // evaluation: PG_REDUCE_NCCL (ncclAllReduce) or PG_REDUCE_FIXED_ORDER
+  // (rank-order sum on the first device, bit-reproducible).
+  std::vector<int> devices;
+  int reduce_mode = PG_REDUCE_NCCL;
+};
+
+// clock.hpp:140-152 (likelihood part of the unconstrained gradient) and
+// clock.hpp:199-213 (node_time_gradient)
+struct ClockGradient {
+  double log_likelihood = 0.0;
+  double dlog_mu = 0.0;                // sum_i b_i g_i
+  std::vector<double> dlog_epsilon;    // b_i g_i, entry node-1
+  std::vector<double> node_time;       // d logL / d t_k, k = N+1..2N-1 at entry k-N-1
 };
 
 // engine.hpp:39-45
@@ -216,7 +233,15 @@ class LikelihoodEngine {
     o.disable_rescaling = options.disable_rescaling;
     o.device = options.device;
     o.capture_partials = options.capture_partials ? 1 : 0;
-    check(pg_create(&o, &h_));
+    // the handle is owned by a guard until construction finishes, so a
+    // setter that throws does not leak the engine and its device buffers
+    pg_engine* raw = nullptr;
+    if (options.devices.empty())
+      check(pg_create(&o, &raw));
+    else
+      check(pg_create_multi(&o, int(options.devices.size()), options.devices.data(), options.reduce_mode, &raw));
+    std::unique_ptr<pg_engine, void (*)(pg_engine*)> guard(raw, pg_destroy);
+    h_ = raw;
     std::vector<int32_t> ch(size_t(2 * (tree.node_count() + 1)));
     for (int i = 0; i <= tree.node_count(); ++i) {
       ch[size_t(2 * i)] = tree.children[size_t(i)][0];
@@ -231,6 +256,7 @@ class LikelihoodEngine {
     check(pg_set_categories(h_, categories_.count(), categories_.rates.data(), categories_.probs.data()));
     std::vector<double> b(tree.branch_length.begin() + 1, tree.branch_length.begin() + tree.node_count());
     set_branch_lengths(b);
+    guard.release();
     patterns_ = alignment.pattern_count();
     states_ = m;
     tip_codes_ = std::move(codes);
@@ -269,6 +295,23 @@ class LikelihoodEngine {
   // clock.hpp:146-152 / cli.hpp:437-438: d logL / d r_i = dt_i g_i
   GradientReport rate_gradient(bool with_hessian_diagonal = false) {
     return eval(PG_EVAL_RATE_GRAD | (with_hessian_diagonal ? PG_EVAL_HESS : 0));
+  }
+  // The relaxed-clock chain rule on the GPU at the current lengths
+  // b_i = r_i dt_i; rates r_i = mu eps_i (nullptr: b_i / dt_i from the
+  // clock durations).
+  ClockGradient clock_gradient(const std::vector<double>* rates = nullptr) {
+    ClockGradient c;
+    c.dlog_epsilon.assign(size_t(tree_.branch_count()), 0.0);
+    c.node_time.assign(size_t(tree_.tip_count - 1), 0.0);
+    if (rates && int(rates->size()) != tree_.branch_count()) throw std::invalid_argument("clock: need one rate per branch");
+    check(pg_clock_gradient(h_, rates ? rates->data() : nullptr, &c.log_likelihood, &c.dlog_mu, c.dlog_epsilon.data(),
+                            c.node_time.data()));
+    return c;
+  }
+  int shard_count() const {
+    int n = 1;
+    check(pg_group_info(h_, &n, nullptr, nullptr));
+    return n;
   }
   pg_engine* handle() { return h_; }
 

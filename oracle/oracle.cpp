@@ -1773,11 +1773,13 @@ int orc_engine_new(void* tree, void* aln, void* model, int L, const double* rate
   const int P = h->aln.pattern_count();
   if (nblocks < 1) nblocks = 1;
   if (nblocks > P) nblocks = std::max(1, P);
-  for (int b = 0; b < nblocks; ++b) {
-    const int p0 = int(int64_t(P) * b / nblocks), p1 = int(int64_t(P) * (b + 1) / nblocks);
-    h->blocks.push_back(std::make_unique<Engine>(h->tree, h->aln, *h->model, cats, opt, p0, p1 - p0));
-    h->blocks.back()->p0_report = p0;
-  }
+  // block engines are built concurrently (their per-node grids dominate setup)
+  h->blocks.resize(size_t(nblocks));
+  run_blocks(h, [&](size_t b) {
+    const int p0 = int(int64_t(P) * int64_t(b) / nblocks), p1 = int(int64_t(P) * int64_t(b + 1) / nblocks);
+    h->blocks[b] = std::make_unique<Engine>(h->tree, h->aln, *h->model, cats, opt, p0, p1 - p0);
+    h->blocks[b]->p0_report = p0;
+  });
   *out = h;
   return 0;
   ORC_CATCH

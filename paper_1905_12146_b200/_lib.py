@@ -20,6 +20,9 @@ PG_ERR_LOGIC = 3
 PG_ERR_NEWICK = 4
 PG_ERR_CUDA = 5
 PG_ERR_NOT_SUPPORTED = 6
+PG_ERR_NCCL = 7
+REDUCE_NCCL = 0
+REDUCE_FIXED_ORDER = 1
 
 EVAL_LOGL = 1
 EVAL_GRAD = 2
@@ -37,9 +40,9 @@ EXPORTS = [
     "pg_evaluate_device", "pg_check_errors", "pg_set_stream", "pg_get_partials", "pg_get_site_log_likelihoods",
     "pg_node_visits", "pg_reset_node_visits", "pg_invalidate_caches", "pg_engine_info", "pg_last_walk_ms",
     "pg_timing", "pg_engine_variant",
+    "pg_create_multi", "pg_group_info", "pg_clock_gradient",
     "pg_newick_parse", "pg_compress_codes", "pg_compress_result", "pg_compress_free", "pg_compress_codes_gpu",
     "pg_compress_result_gpu", "pg_compress_free_gpu", "pg_discrete_gamma",
-    "pg_synth_create", "pg_synth_tree", "pg_synth_model", "pg_synth_patterns", "pg_synth_free",
 ]
 
 
@@ -78,6 +81,10 @@ class NotSupported(PgError, NotImplementedError):
     pass
 
 
+class NcclFailure(PgError, RuntimeError):
+    pass
+
+
 _ERRORS = {
     PG_ERR_INVALID_ARGUMENT: InvalidArgument,
     PG_ERR_RUNTIME: RuntimeFailure,
@@ -85,6 +92,7 @@ _ERRORS = {
     PG_ERR_NEWICK: NewickError,
     PG_ERR_CUDA: CudaFailure,
     PG_ERR_NOT_SUPPORTED: NotSupported,
+    PG_ERR_NCCL: NcclFailure,
 }
 
 
@@ -96,24 +104,6 @@ class Options(C.Structure):
         ("device", C.c_int),
         ("capture_partials", C.c_int),
         ("reserved", C.c_int * 8),
-    ]
-
-
-class SynthSpec(C.Structure):
-    _fields_ = [
-        ("tips", C.c_int),
-        ("model_kind", C.c_int),
-        ("categories", C.c_int),
-        ("gamma_alpha", C.c_double),
-        ("sites", C.c_int64),
-        ("branch_mean", C.c_double),
-        ("clock", C.c_int),
-        ("dt_mean", C.c_double),
-        ("rate_scale", C.c_double),
-        ("rate_sd", C.c_double),
-        ("gap_fraction", C.c_double),
-        ("seed", C.c_uint64),
-        ("threads", C.c_int),
     ]
 
 
@@ -170,6 +160,9 @@ def _declare(L):
         "pg_last_walk_ms": (I, [P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "pg_timing": (I, [P, I, C.POINTER(I), C.POINTER(D), C.POINTER(D)]),
         "pg_engine_variant": (I, [P]),
+        "pg_create_multi": (I, [C.POINTER(Options), I, C.POINTER(I), I, C.POINTER(P)]),
+        "pg_group_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
+        "pg_clock_gradient": (I, [P, PD, PD, PD, PD, PD]),
         "pg_newick_parse": (I, [C.c_char_p, C.POINTER(I), PI32, PI32, PD, PI32, C.c_char_p, C.c_int64]),
         "pg_compress_codes": (I, [I, C.c_int64, PI32, I, C.POINTER(P), C.POINTER(I)]),
         "pg_compress_result": (I, [P, PI32, PI64, PI32]),
@@ -178,11 +171,6 @@ def _declare(L):
         "pg_compress_result_gpu": (I, [P, P, PI64, PI32, C.POINTER(C.c_float)]),
         "pg_compress_free_gpu": (None, [P]),
         "pg_discrete_gamma": (I, [D, I, PD, PD]),
-        "pg_synth_create": (I, [C.POINTER(SynthSpec), C.POINTER(P), C.POINTER(I), C.POINTER(I)]),
-        "pg_synth_tree": (I, [P, PI32, PI32, PI32, PD, PD, PD]),
-        "pg_synth_model": (I, [P, PD, PD, C.POINTER(I), PD, PD]),
-        "pg_synth_patterns": (I, [P, PI8, PI64]),
-        "pg_synth_free": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

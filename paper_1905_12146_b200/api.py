@@ -450,6 +450,21 @@ class EngineOptions:
     disable_rescaling: bool = False
     device: int = 0
     capture_partials: bool = False
+    # multi-GPU from one process (pg_create_multi): shard the patterns over
+    # these devices; reduce "nccl" (ncclAllReduce) or "fixed" (rank-order sum
+    # on the first device, bit-reproducible; repeated devices allowed)
+    devices: Optional[Sequence[int]] = None
+    reduce: str = "nccl"
+
+
+@dataclass
+class ClockGradient:
+    """Likelihood part of RelaxedClockPosterior::gradient (clock.hpp:140-152)
+    and node_time_gradient (clock.hpp:199-213)."""
+    log_likelihood: float = 0.0
+    dlog_mu: float = 0.0                                                 # sum_i b_i g_i
+    dlog_epsilon: np.ndarray = field(default_factory=lambda: np.zeros(0))  # b_i g_i
+    node_time: np.ndarray = field(default_factory=lambda: np.zeros(0))     # [N-1], nodes N+1..2N-1
 
 
 @dataclass
@@ -496,7 +511,14 @@ class LikelihoodEngine:
         o.device = int(opts.device)
         o.capture_partials = int(opts.capture_partials)
         h = C.c_void_p()
-        check(L.pg_create(C.byref(o), C.byref(h)))
+        if opts.devices:
+            if opts.reduce not in ("nccl", "fixed"):
+                raise InvalidArgument("engine: reduce must be 'nccl' or 'fixed'")
+            devs = (C.c_int * len(opts.devices))(*[int(d) for d in opts.devices])
+            check(L.pg_create_multi(C.byref(o), len(opts.devices), devs,
+                                    _L.REDUCE_NCCL if opts.reduce == "nccl" else _L.REDUCE_FIXED_ORDER, C.byref(h)))
+        else:
+            check(L.pg_create(C.byref(o), C.byref(h)))
         self._h = h
         children = np.ascontiguousarray(tree.children.reshape(-1), np.int32)
         check(L.pg_set_topology(h, tree.tip_count, ptr(i32(tree.parent), C.c_int32), ptr(children, C.c_int32),
@@ -595,6 +617,26 @@ class LikelihoodEngine:
         return GradientReport(ll, g, h if with_hessian_diagonal else np.zeros(0), self._aln.pattern_count(),
                               self._cats.count())
 
+    def clock_gradient(self, rates=None) -> ClockGradient:
+        """clock.hpp:140-152 / :199-213 on the GPU at the current lengths
+        b_i = r_i dt_i: d logL/d log eps_i = b_i g_i, d logL/d log mu =
+        sum_i b_i g_i (fixed order), d logL/d t_k (internal nodes).  `rates`
+        r_i = mu eps_i; None derives them as b_i / dt_i from the durations."""
+        r = None if rates is None else f64(rates)
+        if r is not None and r.shape != (self._B,):
+            raise InvalidArgument("clock: need one rate per branch")
+        ll, mu = C.c_double(), C.c_double()
+        eps = np.zeros(self._B)
+        node = np.zeros(self._tree.tip_count - 1)
+        check(lib().pg_clock_gradient(self._h, None if r is None else ptr(r, C.c_double), C.byref(ll), C.byref(mu),
+                                      ptr(eps, C.c_double), ptr(node, C.c_double)))
+        return ClockGradient(ll.value, mu.value, eps, node)
+
+    def group_info(self):
+        n, v, r = C.c_int(), C.c_int(), C.c_int()
+        check(lib().pg_group_info(self._h, C.byref(n), C.byref(v), C.byref(r)))
+        return {"shards": n.value, "nccl_version": v.value, "reduce": ["nccl", "fixed"][r.value]}
+
     def site_log_likelihoods(self):
         out = np.zeros(self._aln.pattern_count())
         check(lib().pg_get_site_log_likelihoods(self._h, ptr(out, C.c_double)))
@@ -666,16 +708,20 @@ def branch_lengths_from_clock(tree: Tree, mu: float, epsilon) -> np.ndarray:
     return mu * eps * (tree.node_time[i] - tree.node_time[tree.parent[i]])
 
 
-def node_time_gradient(tree: Tree, rates, branch_gradient) -> np.ndarray:
-    """clock.hpp:199-213: d logL / d t_k = r_k g_k - sum_children r_c g_c."""
-    r = f64(rates)
-    g = f64(branch_gradient)
-    out = np.zeros(tree.tip_count - 1)
-    for node in range(tree.tip_count + 1, tree.node_count() + 1):
-        v = 0.0
-        if node != tree.root():
-            v += r[node - 1] * g[node - 1]
-        for c in tree.children[node]:
-            v -= r[c - 1] * g[c - 1]
-        out[node - tree.tip_count - 1] = v
-    return out
+def node_time_gradient(engine: "LikelihoodEngine", tree: Tree, mu: float, epsilon) -> np.ndarray:
+    """RelaxedClockPosterior::node_time_gradient (clock.hpp:199-213): sets the
+    engine's lengths from the clock (b_i = mu eps_i dt_i), evaluates the
+    branch gradient and returns d logL / d t_k = r_k g_k [k non-root] -
+    sum_children r_c g_c for the internal nodes N+1..2N-1 (computed on the GPU)."""
+    eps = f64(epsilon)
+    engine.set_branch_lengths(branch_lengths_from_clock(tree, mu, eps))
+    return engine.clock_gradient(mu * eps).node_time
+
+
+def clock_likelihood_gradient(engine: "LikelihoodEngine", tree: Tree, mu: float, epsilon):
+    """Likelihood part of RelaxedClockPosterior::gradient in the unconstrained
+    space (clock.hpp:140-152): returns (d logL/d log mu, d logL/d log eps)."""
+    eps = f64(epsilon)
+    engine.set_branch_lengths(branch_lengths_from_clock(tree, mu, eps))
+    cg = engine.clock_gradient(mu * eps)
+    return cg.dlog_mu, cg.dlog_epsilon

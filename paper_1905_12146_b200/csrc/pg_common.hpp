@@ -22,6 +22,9 @@ struct NewickError : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 struct NotSupported : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -40,6 +43,9 @@ int guarded(F&& f) {
   } catch (const CudaError& e) {
     set_last_error(e.what());
     return PG_ERR_CUDA;
+  } catch (const NcclError& e) {
+    set_last_error(e.what());
+    return PG_ERR_NCCL;
   } catch (const NotSupported& e) {
     set_last_error(e.what());
     return PG_ERR_NOT_SUPPORTED;

@@ -4,6 +4,8 @@
 // contract, cache semantics (engine.hpp:116-130, :146-162), node-visit
 // instrumentation and error messages; the arithmetic runs on the GPU only.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is dlopen()ed by pg_create_multi
 
 #include <algorithm>
 #include <climits>
@@ -61,6 +63,10 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -153,8 +159,10 @@ struct pg_engine {
   int last_launches = 0;
   float last_walk_ms = 0.f, last_total_ms = 0.f;
   int pending_flags = 0;
+  bool err_armed = false;  // d_err holds the flags of evaluations not yet checked
 
   ~pg_engine() {
+    destroy_group();
     for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
     if (h_out) cudaFreeHost(h_out);
     if (h_err) cudaFreeHost(h_err);
@@ -283,18 +291,15 @@ struct pg_engine {
     // warp tile's codes of one tip are 32 aligned bytes (cp.async staging)
     const int64_t pc = (int64_t(np) + 31) / 32 * 32;
     std::vector<uint8_t> col(size_t(N) * size_t(std::max<int64_t>(pc, 32)), 0);
-    bool any_missing = false;
     for (int t = 0; t < N; ++t)
       for (int s = 0; s < np; ++s) {
         const int c = codes[size_t(t) * size_t(np) + size_t(s)];
         if (c < -1 || c >= mm + na) throw std::invalid_argument("alignment: state code out of range");
-        if (c == -1) any_missing = true;
         col[size_t(t) * size_t(pc) + size_t(s)] = uint8_t(c < 0 ? mp + na : c < mm ? c : mp + (c - mm));
       }
     std::vector<double> ambv(size_t(na + 1) * mm, 1.0);
     for (int a = 0; a < na; ++a)
       for (int j = 0; j < mm; ++j) ambv[size_t(a) * mm + j] = ambig[size_t(a) * mm + j];
-    (void)any_missing;
     std::vector<double> wd(static_cast<size_t>(np));
     for (int s = 0; s < np; ++s) {
       if (w[s] < 0) throw std::invalid_argument("alignment: negative pattern weight");
@@ -508,9 +513,14 @@ struct pg_engine {
     use_walkm = m > 4 && !opt.capture_partials && std::getenv("PG_NO_WALKM") == nullptr;
     if (use_walkm) {
       MP = m <= 8 ? 8 : m <= 16 ? 16 : m <= 20 ? 20 : m <= 24 ? 24 : m <= 32 ? 32 : 64;
-      // walkm indexes its tables and per-warp scratch with 32-bit offsets
+      // walkm indexes its tables (TC / QTC columns and the P / P^T fragment
+      // tables, ((node-1) L + l) * max(FRAG, (MP+A) MP)) and its CTA-major
+      // scratch ([node][category][warp][8 MP + 8 exponents]) with 32-bit offsets
       const int64_t lim = int64_t(1) << 31;
-      if (int64_t(B()) * L * (MP + A) * MP >= lim || int64_t(N) * L * (MP * 8 + 4) * 4 >= lim) use_walkm = false;
+      const int64_t KK = MP / 4, frag = KK * ((KK + 1) / 2) * 32;  // WalkMGeom<MP>::FRAG
+      const int64_t table = std::max<int64_t>(frag, int64_t(MP + A) * MP);
+      if (int64_t(B()) * L * table >= lim || int64_t(N) * L * (MP * 8 + 4) * pg_walkm_wpc(MP) >= lim)
+        use_walkm = false;
     }
     if (!use_walkm) MP = m <= 4 ? 4 : m <= 8 ? 8 : m <= 20 ? 20 : m <= 32 ? 32 : 64;
     NC = MP + A;
@@ -574,9 +584,17 @@ struct pg_engine {
     // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents
     const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
-    size_t free_b = 0, total_b = 0;
-    PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = size_t(double(free_b) * 0.6);
+    // The grid (and with it the fixed-order reduction over warp rows) must
+    // not depend on the run-time memory state, or results would not be
+    // bit-reproducible: the scratch budget is a fixed share of
+    // the device's total memory, not of what happens to be free.
+    size_t total_b = 0;
+    {
+      cudaDeviceProp prop{};
+      PG_CUDA(cudaGetDeviceProperties(&prop, device));
+      total_b = prop.totalGlobalMem;
+    }
+    const size_t budget = size_t(double(total_b) * 0.6);
     int cap = int(std::max<size_t>(1, budget / per_warp));
     if (use_walkm) {
       // CTA tiles: 4 warps per tile
@@ -644,7 +662,13 @@ struct pg_engine {
     const bool want_hess = flags & PG_EVAL_HESS;
     if ((flags & PG_EVAL_RATE_GRAD) && !has_dt) throw std::logic_error("engine: rate gradient needs clock durations");
     int launches = 0;
-    PG_CUDA(cudaMemsetAsync(d_err.p, 0x7f, 3 * sizeof(int), stream));  // INT_MAX-ish sentinel
+    // Error flags are sticky until read: several device-side evaluations
+    // (pg_evaluate_device) enqueued back to back report a failure of ANY of
+    // them at the next pg_check_errors, not only of the last one.
+    if (!err_armed) {
+      PG_CUDA(cudaMemsetAsync(d_err.p, 0x7f, 3 * sizeof(int), stream));  // INT_MAX-ish sentinel
+      err_armed = true;
+    }
     PG_CUDA(cudaEventRecord(ev0, stream));
     cudaEvent_t* te = nullptr;
     if (timing) {
@@ -682,18 +706,23 @@ struct pg_engine {
 
   void check_errors() {
     PG_CUDA(cudaStreamSynchronize(stream));
+    err_armed = false;  // the next evaluation starts a fresh error window
     PG_CUDA(cudaEventElapsedTime(&last_walk_ms, ev1, ev2));
     PG_CUDA(cudaEventElapsedTime(&last_total_ms, ev0, ev2));
     if (h_err[2] == 1) throw std::invalid_argument("transition matrix: negative branch length");
     const int nf = h_err[0], uf = h_err[1];
     const int sentinel = 0x7f7f7f7f;
     if (nf != sentinel || uf != sentinel) {
-      if (nf <= uf) throw std::runtime_error("engine: non-finite partial at pattern " + std::to_string(nf));
-      throw std::runtime_error("engine: site likelihood underflowed to zero at pattern " + std::to_string(uf));
+      // pattern_offset: index of this shard's first pattern in a multi-device group
+      if (nf <= uf)
+        throw std::runtime_error("engine: non-finite partial at pattern " + std::to_string(int64_t(nf) + pattern_offset));
+      throw std::runtime_error("engine: site likelihood underflowed to zero at pattern " +
+                               std::to_string(int64_t(uf) + pattern_offset));
     }
   }
 
-  void evaluate(int flags, double* ll_out, double* g_out, double* h_out_) {
+  // Cache test of engine.hpp:146-162 (after the FORCE / REQUIRE_POST rules).
+  bool begin_evaluate(int flags) {
     if ((flags & PG_EVAL_REQUIRE_POST) && !post_valid)
       throw std::logic_error("engine: pre-order pass requires a current post-order pass");
     if (flags & PG_EVAL_FORCE) {
@@ -704,40 +733,85 @@ struct pg_engine {
     const bool want_hess = flags & PG_EVAL_HESS;
     const bool rate = flags & PG_EVAL_RATE_GRAD;
     const bool post_pass = flags & PG_EVAL_POST_PASS;
-    const bool cached = want_grad ? (pre_valid && post_valid && (!want_hess || hess_valid) && rate == rate_grad)
-                                  : (post_pass ? post_valid : ll_valid);
-    if (!cached) {
-      enqueue(flags, nullptr);
-      const int width = want_hess ? accw : (want_grad ? 1 + B() : 1);
-      PG_CUDA(cudaMemcpyAsync(h_out, d_out.p, size_t(width) * sizeof(double), cudaMemcpyDeviceToHost, stream));
-      try {
-        check_errors();
-      } catch (...) {
-        invalidate();
-        throw;
-      }
-      logl = h_out[0];
-      ll_valid = true;
-      if (want_grad) {
-        // reference: post visits only when the post cache was stale
-        visits += uint64_t(post_valid ? 0 : 2 * N - 1) + uint64_t(2 * N - 1);
-        grad.assign(h_out + 1, h_out + 1 + B());
-        if (want_hess) hess.assign(h_out + 1 + B(), h_out + 1 + 2 * B());
-        post_valid = pre_valid = true;
-        hess_valid = want_hess;
-        rate_grad = rate;
-      } else if (post_pass) {
-        visits += uint64_t(2 * N - 1);  // post_order_pass (engine.hpp:188)
-        post_valid = true;
-        pre_valid = hess_valid = false;
-      } else {
-        visits += uint64_t(2 * N - 1);  // scratch likelihood route (engine.hpp:308-309)
-      }
+    return want_grad ? (pre_valid && post_valid && (!want_hess || hess_valid) && rate == rate_grad)
+                     : (post_pass ? post_valid : ll_valid);
+  }
+  static int out_width(int flags, int B) {
+    const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
+    return (flags & PG_EVAL_HESS) ? 1 + 2 * B : (want_grad ? 1 + B : 1);
+  }
+  // Waits for an enqueued evaluation, raises its errors and moves the cache
+  // flags / visit counters like the reference's passes; `res` (host) holds
+  // [logL, g, h] of the evaluation (for a group shard: the reduced result).
+  void finish_evaluate(int flags, const double* res) {
+    const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
+    const bool want_hess = flags & PG_EVAL_HESS;
+    try {
+      check_errors();
+    } catch (...) {
+      invalidate();
+      throw;
     }
+    if (res) {
+      logl = res[0];
+      if (want_grad) grad.assign(res + 1, res + 1 + B());
+      if (want_hess) hess.assign(res + 1 + B(), res + 1 + 2 * B());
+    }
+    ll_valid = true;
+    if (want_grad) {
+      // reference: post visits only when the post cache was stale
+      visits += uint64_t(post_valid ? 0 : 2 * N - 1) + uint64_t(2 * N - 1);
+      post_valid = pre_valid = true;
+      hess_valid = want_hess;
+      rate_grad = flags & PG_EVAL_RATE_GRAD;
+    } else if (flags & PG_EVAL_POST_PASS) {
+      visits += uint64_t(2 * N - 1);  // post_order_pass (engine.hpp:188)
+      post_valid = true;
+      pre_valid = hess_valid = false;
+    } else {
+      visits += uint64_t(2 * N - 1);  // scratch likelihood route (engine.hpp:308-309)
+    }
+  }
+  void copy_out(int flags, double* ll_out, double* g_out, double* h_out_) const {
+    const bool want_grad = flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
     if (ll_out) *ll_out = logl;
     if (want_grad && g_out) std::copy(grad.begin(), grad.end(), g_out);
-    if (want_hess && h_out_) std::copy(hess.begin(), hess.end(), h_out_);
+    if ((flags & PG_EVAL_HESS) && h_out_) std::copy(hess.begin(), hess.end(), h_out_);
   }
+
+  void evaluate(int flags, double* ll_out, double* g_out, double* h_out_) {
+    if (!shards.empty()) {
+      group_evaluate(flags);
+    } else if (!begin_evaluate(flags)) {
+      enqueue(flags, nullptr);
+      PG_CUDA(cudaMemcpyAsync(h_out, d_out.p, size_t(out_width(flags, B())) * sizeof(double), cudaMemcpyDeviceToHost,
+                              stream));
+      finish_evaluate(flags, h_out);
+    }
+    copy_out(flags, ll_out, g_out, h_out_);
+  }
+
+  // ------------------------------------------------ multi-device group
+  // pg_create_multi: this object only holds the group; the work runs on one
+  // single-device engine per entry of the device list, each owning a
+  // contiguous block of patterns, and one reduction of
+  // [logL, g, h] per evaluation (NCCL all-reduce, or a fixed rank-order sum).
+  std::vector<std::unique_ptr<pg_engine>> shards;
+  std::vector<int> shard_p0;
+  int reduce_mode = PG_REDUCE_NCCL;
+  int64_t pattern_offset = 0;
+  std::vector<void*> nccl_comms;  // ncclComm_t per shard
+  std::vector<DevBuf<double>> shard_out;  // per shard: [1 + 2B] on its device
+  DevBuf<double> d_gather;                // fixed-order mode: G x (1 + 2B) on shard 0's device
+  std::vector<double> group_res;
+  bool is_group() const { return !shards.empty(); }
+  void group_evaluate(int flags);
+  void destroy_group();
+
+  // ------------------------------------------------ clock chain rule
+  DevBuf<int> d_children;
+  DevBuf<double> d_clk, d_cg, d_crates;
+  void clock_gradient(const double* rates, double* ll, double* dlog_mu, double* dlog_eps, double* dnode);
 };
 
 namespace {
@@ -878,6 +952,175 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
                            stream));
 }
 
+
+// ======================================================= NCCL (dlopen)
+namespace {
+struct NcclApi {
+  void* so = nullptr;
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*get_version)(int*) = nullptr;
+  int version = 0;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.so) return api;
+  // the process may already hold torch's copy (same soname): dlopen returns it
+  void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!so) throw NcclError(std::string("nccl: cannot load libnccl.so.2: ") + dlerror());
+  auto sym = [&](const char* n) {
+    void* f = dlsym(so, n);
+    if (!f) throw NcclError(std::string("nccl: missing symbol ") + n);
+    return f;
+  };
+  api.comm_init_all = reinterpret_cast<decltype(api.comm_init_all)>(sym("ncclCommInitAll"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
+  api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
+  api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+  api.get_version = reinterpret_cast<decltype(api.get_version)>(sym("ncclGetVersion"));
+  api.get_version(&api.version);
+  api.so = so;
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NcclError(std::string("nccl: ") + what + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+void pg_engine::destroy_group() {
+  for (void* c : nccl_comms)
+    if (c) nccl().comm_destroy(static_cast<ncclComm_t>(c));
+  nccl_comms.clear();
+  shard_out.clear();
+  shards.clear();
+}
+
+void pg_engine::group_evaluate(int flags) {
+  const int G = int(shards.size());
+  bool all_cached = true;
+  for (auto& sh : shards) {
+    sh->set_device();
+    all_cached = sh->begin_evaluate(flags) && all_cached;
+  }
+  if (all_cached) return;  // every shard caches the reduced result
+  const int Bn = shards[0]->B();
+  const int width = out_width(flags, Bn);
+  for (int r = 0; r < G; ++r) {
+    pg_engine& sh = *shards[size_t(r)];
+    sh.set_device();
+    shard_out[size_t(r)].ensure(size_t(1 + 2 * Bn));
+    sh.enqueue(flags | PG_EVAL_FORCE, shard_out[size_t(r)].p);
+  }
+  pg_engine& s0 = *shards[0];
+  if (reduce_mode == PG_REDUCE_NCCL) {
+    NcclApi& api = nccl();
+    nccl_check(api.group_start(), "ncclGroupStart");
+    for (int r = 0; r < G; ++r) {
+      pg_engine& sh = *shards[size_t(r)];
+      sh.set_device();
+      nccl_check(api.all_reduce(shard_out[size_t(r)].p, shard_out[size_t(r)].p, size_t(width), ncclFloat64, ncclSum,
+                                static_cast<ncclComm_t>(nccl_comms[size_t(r)]), sh.stream),
+                 "ncclAllReduce");
+    }
+    nccl_check(api.group_end(), "ncclGroupEnd");
+    s0.set_device();
+    PG_CUDA(cudaMemcpyAsync(s0.h_out, shard_out[0].p, size_t(width) * sizeof(double), cudaMemcpyDeviceToHost,
+                            s0.stream));
+  } else {
+    // fixed rank-order sum on the first device: bit-reproducible
+    s0.set_device();
+    d_gather.ensure(size_t(G) * size_t(width));
+    for (int r = 0; r < G; ++r) {
+      pg_engine& sh = *shards[size_t(r)];
+      sh.set_device();
+      PG_CUDA(cudaMemcpyPeerAsync(d_gather.p + size_t(r) * width, s0.device, shard_out[size_t(r)].p, sh.device,
+                                  size_t(width) * sizeof(double), sh.stream));
+      if (r > 0) {
+        cudaEvent_t ev;
+        PG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PG_CUDA(cudaEventRecord(ev, sh.stream));
+        s0.set_device();
+        PG_CUDA(cudaStreamWaitEvent(s0.stream, ev, 0));
+        PG_CUDA(cudaEventDestroy(ev));  // released once the wait has been satisfied
+      }
+    }
+    s0.set_device();
+    pgk::shard_sum_kernel<<<(width + 255) / 256, 256, 0, s0.stream>>>(d_gather.p, G, width, s0.d_out.p);
+    PG_CUDA(cudaGetLastError());
+    PG_CUDA(cudaMemcpyAsync(s0.h_out, s0.d_out.p, size_t(width) * sizeof(double), cudaMemcpyDeviceToHost, s0.stream));
+  }
+  // wait for every shard, raise the first error, cache the reduced result
+  std::exception_ptr first;
+  s0.set_device();
+  try {
+    PG_CUDA(cudaStreamSynchronize(s0.stream));
+  } catch (...) {
+    first = std::current_exception();
+  }
+  group_res.assign(s0.h_out, s0.h_out + width);
+  for (auto& sh : shards) {
+    try {
+      sh->set_device();
+      sh->finish_evaluate(flags, group_res.data());
+    } catch (...) {
+      if (!first) first = std::current_exception();
+    }
+  }
+  if (first) {
+    for (auto& sh : shards) sh->invalidate();
+    std::rethrow_exception(first);
+  }
+}
+
+void pg_engine::clock_gradient(const double* r_host, double* ll_out, double* dlog_mu, double* dlog_eps,
+                               double* dnode) {
+  pg_engine& pe = is_group() ? *shards[0] : *this;
+  if (!r_host && !pe.has_dt) throw std::logic_error("engine: clock gradient needs rates or clock durations");
+  evaluate(PG_EVAL_GRAD, ll_out, nullptr, nullptr);
+  const int Bn = pe.B(), Nn = pe.N;
+  pe.set_device();
+  d_children.upload(pe.children.data(), pe.children.size(), pe.stream);
+  d_cg.upload(pe.grad.data(), pe.grad.size(), pe.stream);
+  if (r_host) {
+    for (int i = 0; i < Bn; ++i)
+      if (!std::isfinite(r_host[i])) throw std::invalid_argument("clock: rates must be finite");
+    d_crates.upload(r_host, size_t(Bn), pe.stream);
+  }
+  d_clk.ensure(size_t(1 + Bn + Nn - 1));
+  pgk::clock_kernel<<<1, pgk::kClockThreads, 0, pe.stream>>>(d_cg.p, pe.d_blen.p, r_host ? d_crates.p : nullptr,
+                                                             pe.d_dt.p, d_children.p, Nn, d_clk.p);
+  PG_CUDA(cudaGetLastError());
+  std::vector<double> h(size_t(1 + Bn + Nn - 1));
+  PG_CUDA(cudaMemcpyAsync(h.data(), d_clk.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, pe.stream));
+  PG_CUDA(cudaStreamSynchronize(pe.stream));
+  if (dlog_mu) *dlog_mu = h[0];
+  if (dlog_eps) std::copy(h.begin() + 1, h.begin() + 1 + Bn, dlog_eps);
+  if (dnode) std::copy(h.begin() + 1 + Bn, h.end(), dnode);
+}
+
+namespace {
+template <class F>
+void each(pg_engine* e, F&& f) {
+  if (e->is_group())
+    for (auto& sh : e->shards) f(sh.get());
+  else
+    f(e);
+}
+pg_engine* primary(pg_engine* e) { return e->is_group() ? e->shards[0].get() : e; }
+const pg_engine* primary(const pg_engine* e) { return e->is_group() ? e->shards[0].get() : e; }
+void single_only(const pg_engine* e, const char* what) {
+  if (e->is_group()) throw NotSupported(std::string(what) + ": not supported on a multi-device group");
+}
+}  // namespace
+
 // ============================================================== C-ABI
 extern "C" {
 
@@ -905,58 +1148,146 @@ int pg_create(const pg_options* opt, pg_engine** out) {
 
 void pg_destroy(pg_engine* e) { delete e; }
 
+int pg_create_multi(const pg_options* opt, int device_count, const int* devices, int reduce_mode, pg_engine** out) {
+  return guarded([&] {
+    if (device_count < 1 || !devices) throw std::invalid_argument("engine: need at least one device");
+    if (reduce_mode != PG_REDUCE_NCCL && reduce_mode != PG_REDUCE_FIXED_ORDER)
+      throw std::invalid_argument("engine: unknown reduce mode");
+    std::vector<int> devs(devices, devices + device_count);
+    if (reduce_mode == PG_REDUCE_NCCL) {
+      std::vector<int> sorted = devs;
+      std::sort(sorted.begin(), sorted.end());
+      if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+        throw std::invalid_argument("engine: the NCCL reduction needs distinct devices (use PG_REDUCE_FIXED_ORDER)");
+    }
+    auto g = std::make_unique<pg_engine>();
+    if (opt) g->opt = *opt;
+    else pg_default_options(&g->opt);
+    if (g->opt.capture_partials) throw NotSupported("engine: partial capture is not supported on a multi-device group");
+    g->reduce_mode = reduce_mode;
+    g->device = devs[0];
+    for (int d : devs) {
+      pg_options o = g->opt;
+      o.device = d;
+      pg_engine* sh = nullptr;
+      if (pg_create(&o, &sh) != PG_OK) throw CudaError(pg_last_error());
+      g->shards.emplace_back(sh);
+    }
+    g->shard_out.resize(devs.size());
+    if (reduce_mode == PG_REDUCE_NCCL) {
+      g->nccl_comms.assign(devs.size(), nullptr);
+      std::vector<ncclComm_t> comms(devs.size());
+      nccl_check(nccl().comm_init_all(comms.data(), device_count, devs.data()), "ncclCommInitAll");
+      for (size_t i = 0; i < comms.size(); ++i) g->nccl_comms[i] = comms[i];
+    } else {
+      // peer access lets the gather copies go over NVLink directly
+      for (int d : devs)
+        for (int d2 : devs)
+          if (d != d2) {
+            int ok = 0;
+            cudaDeviceCanAccessPeer(&ok, d, d2);
+            if (ok) {
+              cudaSetDevice(d);
+              const cudaError_t r = cudaDeviceEnablePeerAccess(d2, 0);
+              if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled) PG_CUDA(r);
+              cudaGetLastError();
+            }
+          }
+    }
+    *out = g.release();
+  });
+}
+
+int pg_group_info(const pg_engine* e, int* shard_count, int* nccl_version, int* reduce_mode) {
+  return guarded([&] {
+    if (shard_count) *shard_count = e->is_group() ? int(e->shards.size()) : 1;
+    if (nccl_version) *nccl_version = (e->is_group() && e->reduce_mode == PG_REDUCE_NCCL) ? nccl().version : 0;
+    if (reduce_mode) *reduce_mode = e->reduce_mode;
+  });
+}
+
+int pg_clock_gradient(pg_engine* e, const double* rates, double* log_likelihood, double* dlog_mu, double* dlog_eps,
+                      double* dnode_time) {
+  return guarded([&] { e->clock_gradient(rates, log_likelihood, dlog_mu, dlog_eps, dnode_time); });
+}
+
 int pg_set_topology(pg_engine* e, int tip_count, const int32_t* parent, const int32_t* children,
                     const int32_t* post_order) {
-  return guarded([&] { e->set_topology(tip_count, parent, children, post_order); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_topology(tip_count, parent, children, post_order); }); });
 }
 
 int pg_set_patterns(pg_engine* e, int state_count, int pattern_count, const int8_t* codes, int ambiguity_count,
                     const double* ambiguity, const int64_t* weights) {
-  return guarded([&] { e->set_patterns(state_count, pattern_count, codes, ambiguity_count, ambiguity, weights); });
+  return guarded([&] {
+    if (!e->is_group()) {
+      e->set_patterns(state_count, pattern_count, codes, ambiguity_count, ambiguity, weights);
+      return;
+    }
+    // contiguous pattern blocks, shard r: [floor(r P / G), floor((r+1) P / G))
+    const int G = int(e->shards.size());
+    const int N = e->shards[0]->N;
+    if (pattern_count < 0) throw std::invalid_argument("alignment: negative pattern count");
+    for (int r = 0; r < G; ++r) {
+      const int p0 = int(int64_t(pattern_count) * r / G), p1 = int(int64_t(pattern_count) * (r + 1) / G);
+      std::vector<int8_t> c(size_t(N) * size_t(p1 - p0));
+      for (int t = 0; t < N; ++t)
+        std::copy(codes + size_t(t) * size_t(pattern_count) + size_t(p0),
+                  codes + size_t(t) * size_t(pattern_count) + size_t(p1), c.begin() + ptrdiff_t(size_t(t) * (p1 - p0)));
+      e->shards[size_t(r)]->set_patterns(state_count, p1 - p0, c.data(), ambiguity_count, ambiguity, weights + p0);
+      e->shards[size_t(r)]->pattern_offset = p0;
+    }
+  });
 }
 
 int pg_set_model(pg_engine* e, int state_count, const double* q, const double* pi, int reversible) {
-  return guarded([&] { e->set_model(state_count, q, pi, reversible); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_model(state_count, q, pi, reversible); }); });
 }
 
 int pg_set_branch_generator(pg_engine* e, int branch, const double* q) {
-  return guarded([&] { e->set_branch_generator(branch, q); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_branch_generator(branch, q); }); });
 }
 
 int pg_set_categories(pg_engine* e, int category_count, const double* rates, const double* probs) {
-  return guarded([&] { e->set_categories(category_count, rates, probs); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_categories(category_count, rates, probs); }); });
 }
 
 int pg_set_branch_lengths(pg_engine* e, const double* b) {
-  return guarded([&] { e->set_branch_lengths(b); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_branch_lengths(b); }); });
 }
 
 int pg_set_branch_lengths_device(pg_engine* e, const double* b_device) {
-  return guarded([&] { e->set_branch_lengths_device(b_device); });
+  return guarded([&] {
+    single_only(e, "pg_set_branch_lengths_device");
+    e->set_branch_lengths_device(b_device);
+  });
 }
 
 int pg_get_branch_lengths(pg_engine* e, double* b) {
   return guarded([&] {
-    e->set_device();
-    e->sync_host_blen();
-    std::copy(e->blen.begin(), e->blen.end(), b);
+    pg_engine* x = primary(e);
+    x->set_device();
+    x->sync_host_blen();
+    std::copy(x->blen.begin(), x->blen.end(), b);
   });
 }
 
 int pg_set_clock_durations(pg_engine* e, const double* dt) {
-  return guarded([&] { e->set_durations(dt); });
+  return guarded([&] { each(e, [&](pg_engine* x) { x->set_durations(dt); }); });
 }
 
 int pg_evaluate(pg_engine* e, int flags, double* log_likelihood, double* grad, double* hess) {
   return guarded([&] {
-    if ((flags & (PG_EVAL_GRAD | PG_EVAL_RATE_GRAD)) && !grad && (flags & PG_EVAL_GRAD))
+    if ((flags & (PG_EVAL_GRAD | PG_EVAL_RATE_GRAD)) && !grad)
       throw std::invalid_argument("pg_evaluate: gradient requested without an output buffer");
+    if ((flags & PG_EVAL_HESS) && !hess)
+      throw std::invalid_argument("pg_evaluate: Hessian requested without an output buffer");
     e->evaluate(flags, log_likelihood, grad, hess);
   });
 }
 
 int pg_evaluate_device(pg_engine* e, int flags, double* out_device) {
   return guarded([&] {
+    single_only(e, "pg_evaluate_device");
     if (!out_device) throw std::invalid_argument("pg_evaluate_device: null output");
     e->invalidate();
     e->enqueue(flags | PG_EVAL_FORCE, out_device);
@@ -965,6 +1296,7 @@ int pg_evaluate_device(pg_engine* e, int flags, double* out_device) {
 
 int pg_check_errors(pg_engine* e) {
   return guarded([&] {
+    single_only(e, "pg_check_errors");
     const bool grad = e->pending_flags & (PG_EVAL_GRAD | PG_EVAL_HESS | PG_EVAL_RATE_GRAD);
     e->check_errors();
     e->visits += uint64_t(grad ? 2 : 1) * uint64_t(2 * e->N - 1);
@@ -973,6 +1305,7 @@ int pg_check_errors(pg_engine* e) {
 
 int pg_set_stream(pg_engine* e, void* s) {
   return guarded([&] {
+    single_only(e, "pg_set_stream");
     if (e->own_stream && e->stream) {
       PG_CUDA(cudaStreamSynchronize(e->stream));
       PG_CUDA(cudaStreamDestroy(e->stream));
@@ -985,6 +1318,7 @@ int pg_set_stream(pg_engine* e, void* s) {
 int pg_get_partials(pg_engine* e, int node, int category, double* post, double* pre, double* post_scaler,
                     double* pre_scaler) {
   return guarded([&] {
+    single_only(e, "pg_get_partials");
     if (!e->opt.capture_partials) throw std::logic_error("engine: partial capture is disabled");
     if (!e->pre_valid) throw std::logic_error("engine: no current gradient pass to read partials from");
     const int n = 2 * e->N - 1;
@@ -1058,21 +1392,30 @@ int pg_get_partials(pg_engine* e, int node, int category, double* post, double* 
 
 int pg_get_site_log_likelihoods(pg_engine* e, double* out) {
   return guarded([&] {
-    if (!e->ll_valid) throw std::logic_error("engine: no current evaluation");
-    e->set_device();
-    PG_CUDA(cudaMemcpy(out, e->d_site_ll.p, size_t(e->P) * sizeof(double), cudaMemcpyDeviceToHost));
+    int64_t off = 0;
+    each(e, [&](pg_engine* x) {  // shards in pattern order
+      if (!x->ll_valid) throw std::logic_error("engine: no current evaluation");
+      x->set_device();
+      PG_CUDA(cudaMemcpy(out + off, x->d_site_ll.p, size_t(x->P) * sizeof(double), cudaMemcpyDeviceToHost));
+      off += x->P;
+    });
   });
 }
 
-uint64_t pg_node_visits(const pg_engine* e) { return e->visits; }
-void pg_reset_node_visits(pg_engine* e) { e->visits = 0; }
+uint64_t pg_node_visits(const pg_engine* e) { return primary(e)->visits; }
+void pg_reset_node_visits(pg_engine* e) {
+  each(e, [](pg_engine* x) { x->visits = 0; });
+}
 void pg_invalidate_caches(pg_engine* e) {
-  e->invalidate();
-  e->tc_dirty = true;  // the reference recomputes trans_ in every post pass (engine.hpp:197-201)
+  each(e, [](pg_engine* x) {
+    x->invalidate();
+    x->tc_dirty = true;  // the reference recomputes trans_ in every post pass (engine.hpp:197-201)
+  });
 }
 
 int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lanes_per_pattern, int* padded_states) {
   return guarded([&] {
+    e = primary(e);
     if (launches) *launches = e->last_launches;
     if (total_warps) *total_warps = e->TW;
     if (lanes_per_pattern) *lanes_per_pattern = e->G;
@@ -1082,6 +1425,15 @@ int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lan
 
 int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total, double* eval_ms_total) {
   return guarded([&] {
+    if (e->is_group())
+      for (size_t i = 1; i < e->shards.size(); ++i) {  // shard 0 reports below
+        pg_engine* x = e->shards[i].get();
+        x->set_device();
+        PG_CUDA(cudaStreamSynchronize(x->stream));
+        x->tev_used = 0;
+        x->timing = enable != 0;
+      }
+    e = primary(e);
     e->set_device();
     PG_CUDA(cudaStreamSynchronize(e->stream));
     const int n = int(e->tev_used / 3);
@@ -1101,10 +1453,14 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
   });
 }
 
-int pg_engine_variant(const pg_engine* e) { return e->use_walkm ? 2 : e->use_walk4 ? 1 : 0; }
+int pg_engine_variant(const pg_engine* e) {
+  e = primary(e);
+  return e->use_walkm ? 2 : e->use_walk4 ? 1 : 0;
+}
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {
   return guarded([&] {
+    e = primary(e);
     if (walk_ms) *walk_ms = e->last_walk_ms;
     if (total_ms) *total_ms = e->last_total_ms;
   });

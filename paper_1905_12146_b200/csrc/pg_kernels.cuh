@@ -49,6 +49,56 @@ __global__ void __launch_bounds__(32 * kReduceGroups) reduce_kernel(const double
   out[i] = s;
 }
 
+// ------------------------------------------------------- clock chain rule
+// clock.hpp:140-152 (likelihood part of RelaxedClockPosterior::gradient) and
+// clock.hpp:199-213 (node_time_gradient) from one branch gradient g:
+//   dlog_eps[i] = b_i g_i, dlog_mu = sum_i b_i g_i (fixed-order block
+//   reduction), dnode[k] = r_k g_k (non-root) - sum_{c in children} r_c g_c
+// with r_i = rates[i], or b_i / dt_i when rates is null.  One block.
+constexpr int kClockThreads = 512;
+__global__ void __launch_bounds__(kClockThreads)
+    clock_kernel(const double* __restrict__ g, const double* __restrict__ b, const double* __restrict__ rates,
+                 const double* __restrict__ dt, const int* __restrict__ children, int N,
+                 double* __restrict__ out /* [1 + B + N-1]: dlog_mu, dlog_eps, dnode */) {
+  __shared__ double part[kClockThreads];
+  const int B = 2 * N - 2, root = 2 * N - 1;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < B; i += kClockThreads) {
+    const double v = b[i] * g[i];
+    out[1 + i] = v;
+    s += v;
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kClockThreads / 2; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = part[0];
+  auto rg = [&](int node) {
+    const double r = rates ? rates[node - 1] : b[node - 1] / dt[node - 1];
+    return r * g[node - 1];
+  };
+  for (int k = threadIdx.x; k < N - 1; k += kClockThreads) {
+    const int node = N + 1 + k;
+    double v = 0.0;
+    if (node != root) v += rg(node);
+    v -= rg(children[2 * node]);
+    v -= rg(children[2 * node + 1]);
+    out[1 + B + k] = v;
+  }
+}
+
+// Fixed rank-order sum of G shard outputs gathered on one device
+// (bit-reproducible multi-device reduction: sum over shards 0, 1, ..., G-1).
+__global__ void shard_sum_kernel(const double* __restrict__ parts, int G, int width, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < width; i += gridDim.x * blockDim.x) {
+    double s = parts[i];
+    for (int r = 1; r < G; ++r) s += parts[size_t(r) * width + i];
+    out[i] = s;
+  }
+}
+
 // ------------------------------------------------------------------- K1
 struct TcParams {
   const double* blen;   // [B] branch lengths (index node-1)

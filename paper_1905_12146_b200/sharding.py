@@ -67,6 +67,30 @@ class ShardedEngine:
         self.dist.all_reduce(t, group=self.group)
         return t.numpy()
 
+    def set_clock_durations(self, dt):
+        if hasattr(self.local, "set_clock_durations"):
+            self.local.set_clock_durations(dt)
+        self.durations = np.asarray(dt, dtype=np.float64).copy()
+
+    def enqueue_device(self, flags, out):
+        """Asynchronous step of the NCCL path: this rank's evaluation into the
+        CUDA tensor `out` ([logL, g (, h)]) on the current stream, then the
+        all-reduce on the same stream.  pg_check_errors (check_errors) reports
+        a failure of any step enqueued since the last check (sticky flags)."""
+        import torch
+
+        from . import _lib as _L
+
+        L = _L.lib()
+        _L.check(L.pg_set_stream(self.local.handle, torch.cuda.current_stream().cuda_stream))
+        _L.check(L.pg_evaluate_device(self.local.handle, flags, out.data_ptr()))
+        self.dist.all_reduce(out, group=self.group)
+
+    def check_errors(self):
+        from . import _lib as _L
+
+        _L.check(_L.lib().pg_check_errors(self.local.handle))
+
     def _device_eval(self, flags):
         import torch
 
@@ -74,11 +98,8 @@ class ShardedEngine:
 
         width = 1 + self.B * (2 if flags & _L.EVAL_HESS else 1)
         out = torch.zeros(width, dtype=torch.float64, device="cuda")
-        L = _L.lib()
-        _L.check(L.pg_set_stream(self.local.handle, torch.cuda.current_stream().cuda_stream))
-        _L.check(L.pg_evaluate_device(self.local.handle, flags, out.data_ptr()))
-        self.dist.all_reduce(out, group=self.group)
-        _L.check(L.pg_check_errors(self.local.handle))
+        self.enqueue_device(flags, out)
+        self.check_errors()
         return out.cpu().numpy()
 
     def branch_gradient(self, with_hessian_diagonal=False):
@@ -99,6 +120,25 @@ class ShardedEngine:
         return GradientReport(float(v[0]), v[1:1 + self.B].copy(),
                               v[1 + self.B:].copy() if with_hessian_diagonal else np.zeros(0),
                               self.p1 - self.p0, 0)
+
+    def rate_gradient(self, with_hessian_diagonal=False):
+        """d logL / d r_i = dt_i g_i for b_i = r_i dt_i (clock.hpp:146-152,
+        cli.hpp:437-438): on the device path the chain rule runs in the
+        engine's reduction kernel; on the host path it scales the reduced g."""
+        from .api import GradientReport
+
+        if self._device_path:
+            from . import _lib as _L
+
+            v = self._device_eval(_L.EVAL_RATE_GRAD | (_L.EVAL_HESS if with_hessian_diagonal else 0))
+            return GradientReport(float(v[0]), v[1:1 + self.B].copy(),
+                                  v[1 + self.B:].copy() if with_hessian_diagonal else np.zeros(0),
+                                  self.p1 - self.p0, 0)
+        rep = self.branch_gradient(with_hessian_diagonal)
+        dt = self.durations
+        return GradientReport(rep.log_likelihood, dt * rep.branch_gradient,
+                              dt * dt * rep.hessian_diagonal if with_hessian_diagonal else np.zeros(0),
+                              rep.pattern_count, 0)
 
     def log_likelihood(self):
         ll = self.local.log_likelihood()

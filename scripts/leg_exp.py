@@ -3,7 +3,8 @@ API, to see whether per-evaluation time drifts with sustained load."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_1905_12146_b200 import synth, _lib as _L
+from paper_1905_12146_b200 import _lib as _L
+from workloads import synth
 inst = synth.generate("C3", sites=int(os.environ.get("SITES", "1000000")))
 eng = synth.engine_for(inst)
 L = _L.lib()

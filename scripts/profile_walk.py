@@ -6,7 +6,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1905_12146_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")

@@ -6,7 +6,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_1905_12146_b200 import _lib as _L, synth  # noqa: E402
+from paper_1905_12146_b200 import _lib as _L  # noqa: E402
+from workloads import synth  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 inst = synth.generate(cfg)

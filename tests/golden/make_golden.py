@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from oracle import oracle as O  # noqa: E402
-from paper_1905_12146_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 
 
 def from_instance(name, inst, branch_q=()):

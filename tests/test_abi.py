@@ -137,7 +137,7 @@ def test_discrete_gamma_matches_oracle():  # test_substitution.cpp:160-184
 
 
 def test_synthetic_configs_deterministic():
-    from paper_1905_12146_b200 import synth
+    from workloads import synth
 
     a = synth.generate("C2", seed=3, sites=2000)
     b = synth.generate("C2", seed=3, sites=2000, threads=1)

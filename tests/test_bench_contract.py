@@ -55,3 +55,30 @@ def test_device_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["value"] > 0 and cb["single_thread"]["cores"] == 1
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_both_arms_share_config_and_parity_block(tmp_path, monkeypatch):
+    """Identical `config` in both arms; the parity block compares against a
+    full-size fixture only when the instance digest matches."""
+    import numpy as np
+
+    import bench
+    from workloads import synth
+
+    args = bench.parse_args(["--config", "C1"])
+    inst = synth.generate("C1", seed=bench.SEED)
+    cfg = bench.bench_config(args, inst)
+    assert cfg["workload"] == "C1" and cfg["patterns"] == inst.patterns and cfg["sites"] == 1000
+    # parity: fixture with this instance's digest
+    g = np.linspace(-1.0, 1.0, inst.branches)
+    fx = tmp_path / "tests" / "golden"
+    fx.mkdir(parents=True)
+    np.savez(fx / "full_C1.npz", digest=synth.instance_digest(inst), logL=-1234.5, gradient=g,
+             rate_gradient=np.zeros(0), oracle_threads=8)
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    ok = bench.parity_block(args, inst, -1234.5 * (1 + 1e-12), g * (1 + 1e-11))
+    assert ok["match"] and ok["within_1e-9"] and ok["logL_rel"] < 1e-11
+    bad = bench.parity_block(args, inst, -1234.5, g + 1e-3)
+    assert bad["match"] and not bad["within_1e-9"]
+    other = synth.generate("C1", seed=bench.SEED + 1)
+    assert bench.parity_block(args, other, -1.0, g)["match"] is False

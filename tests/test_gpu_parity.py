@@ -13,7 +13,7 @@ from tests.helpers import assert_logl, assert_vec, oracle_for
 pytestmark = pytest.mark.gpu
 
 pg = pytest.importorskip("paper_1905_12146_b200")
-from paper_1905_12146_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCategories,  # noqa: E402
                                        SitePatternAlignment, SubstitutionModel, Tree, discrete_gamma_categories,
                                        parse_fasta, parse_newick)

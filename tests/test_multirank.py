@@ -49,7 +49,7 @@ def _worker(rank, world, port, result_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1905_12146_b200 import synth
+        from workloads import synth
         from paper_1905_12146_b200.api import RateCategories, SitePatternAlignment, SubstitutionModel, Tree
         from paper_1905_12146_b200.sharding import ShardedEngine, shard_range
 
@@ -81,7 +81,7 @@ def test_two_rank_gloo_sharded_gradient():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    from paper_1905_12146_b200 import synth
+    from workloads import synth
     from tests.helpers import oracle_for
 
     inst = synth.generate("C2", seed=5, sites=1500, tips=40)
@@ -115,7 +115,7 @@ def test_single_rank_nccl_device_path():
     import torch
     import torch.distributed as dist
 
-    from paper_1905_12146_b200 import synth
+    from workloads import synth
     from paper_1905_12146_b200.api import RateCategories, SitePatternAlignment, SubstitutionModel, Tree
     from paper_1905_12146_b200.sharding import ShardedEngine
     from tests.helpers import assert_logl, assert_vec, oracle_for
@@ -146,7 +146,7 @@ def _share_worker(rank, world, port, q):
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        from paper_1905_12146_b200 import synth
+        from workloads import synth
 
         inst = synth.generate_shared("C2", rank, world, dist.barrier, tag=f"test{port}", seed=3, sites=700)
         q.put((rank, inst.patterns, int(inst.codes.astype(np.int64).sum()), int(inst.weights.sum()),
@@ -169,9 +169,75 @@ def test_shared_workload_generation():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    from paper_1905_12146_b200 import synth
+    from workloads import synth
 
     ref = synth.generate("C2", seed=3, sites=700)
     want = (ref.patterns, int(ref.codes.astype(np.int64).sum()), int(ref.weights.sum()), float(ref.branch_lengths.sum()))
     for r in res:
         assert r[1:] == want
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's multi-rank e2e step on CPU: shared workload generation,
+    the product ShardedEngine over this rank's block (oracle as the local
+    engine), the clock chain rule (set_clock_durations + rate_gradient)."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1905_12146_b200.sharding import ShardedEngine
+        from workloads import synth
+
+        inst = synth.generate_shared("C3", rank, world, dist.barrier, tag=f"bench{port}", seed=11, sites=900)
+        sh = ShardedEngine(*synth.api_objects(inst), engine_factory=OracleLocal)
+        sh.set_clock_durations(inst.durations)
+        b = inst.branch_rates * inst.durations
+        sh.set_branch_lengths(b)
+        rep = sh.rate_gradient()
+        q.put((rank, rep.log_likelihood, rep.branch_gradient, sh.p1 - sh.p0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_multirank_step_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from tests.helpers import oracle_for
+    from workloads import synth
+
+    inst = synth.generate("C3", seed=11, sites=900)
+    ll, g, _ = oracle_for(inst, blocks=4).branch_gradient(False)
+    assert sum(r[3] for r in results) == inst.patterns
+    for _, rll, rg, _ in results:
+        assert rll == pytest.approx(ll, rel=1e-12)
+        np.testing.assert_allclose(rg, inst.durations * g, rtol=1e-10,
+                                   atol=1e-12 * np.abs(inst.durations * g).max())
+
+
+def test_bench_relaunches_under_torchrun(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N processes on a 127.0.0.1 rendezvous; under
+    torchrun a --gpus / WORLD_SIZE mismatch is an error."""
+    import bench
+
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    args = bench.parse_args(["--gpus", "4", "--steps", "2"])
+    cmd = bench.relaunch_command(args, ["--gpus", "4", "--steps", "2"])
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+    assert bench.relaunch_command(bench.parse_args(["--gpus", "1"]), []) is None
+    assert bench.relaunch_command(bench.parse_args(["--gpus", "4", "--impl", "reference"]), []) is None
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench.relaunch_command(args, []) is None
+    assert bench.main(["--gpus", "4"]) == 2

@@ -3,9 +3,16 @@
 The paper's WNV/LASV/DENV alignments are not available; these generators
 produce inputs with the configs' shapes and value distributions: Yule trees
 numbered like parse_newick, model parameters drawn as the config states,
-forward simulation down the tree (alignment.hpp:243-286 semantics with
-per-block RNG streams so it parallelises), optional gaps, then first-occurrence
-pattern compression.  Input generation only — never inside a timed region.
+forward simulation down the tree (alignment.hpp:243-286), optional gaps, then
+first-occurrence pattern compression.  C1 and C2 are simulated in the
+reference's own draw order (one mt19937_64 stream, so the reference's
+simulate_states regenerates their columns); C3-C5 (10^5..10^6 columns) use
+independent per-block streams so they simulate on every host core.
+
+Input generation only — never inside a timed region.  The native code is
+workloads/_build/libpg_workloads.so, a host library separate from the product
+(libphylograd_b200.so), so the CPU reference arm of bench.py builds the same
+inputs without mapping any product code.
 """
 from __future__ import annotations
 
@@ -14,14 +21,74 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib as _L
-from ._lib import check, lib, ptr
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "_build", "libpg_workloads.so")
+SIM_BLOCKED, SIM_REFERENCE = 0, 1
+
+
+class Spec(C.Structure):
+    _fields_ = [
+        ("tips", C.c_int),
+        ("model_kind", C.c_int),
+        ("categories", C.c_int),
+        ("gamma_alpha", C.c_double),
+        ("sites", C.c_int64),
+        ("branch_mean", C.c_double),
+        ("clock", C.c_int),
+        ("dt_mean", C.c_double),
+        ("rate_scale", C.c_double),
+        ("rate_sd", C.c_double),
+        ("gap_fraction", C.c_double),
+        ("seed", C.c_uint64),
+        ("threads", C.c_int),
+        ("sim", C.c_int),
+    ]
+
+
+_lib = None
+_P, _I, _D = C.c_void_p, C.c_int, C.c_double
+_PD, _PI32, _PI64, _PI8 = C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int8)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(f"workloads: {SO_PATH} is not built; run __graft_entry__.build()")
+        L = C.CDLL(SO_PATH)
+        for name, (res, args) in {
+            "pgw_last_error": (C.c_char_p, []),
+            "pgw_create": (_I, [C.POINTER(Spec), C.POINTER(_P), C.POINTER(_I), C.POINTER(_I)]),
+            "pgw_tree": (_I, [_P, _PI32, _PI32, _PI32, _PD, _PD, _PD]),
+            "pgw_model": (_I, [_P, _PD, _PD, C.POINTER(_I), _PD, _PD]),
+            "pgw_patterns": (_I, [_P, _PI8, _PI64]),
+            "pgw_free": (None, [_P]),
+            "pgw_simulate_states": (_I, [_I, _PI32, _PI32, _I, _PD, _PD, _I, _I, _PD, _PD, _PD, C.c_int64,
+                                         C.c_uint64, _PI8]),
+        }.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc != 0:
+        raise ValueError(lib().pgw_last_error().decode(errors="replace"))
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
 
 # name -> (tips, model_kind, categories, alpha, sites, branch_mean, clock, dt_mean, rate_scale, rate_sd, gaps)
 CONFIGS = {
-    "C1": dict(tips=64, model_kind=0, categories=1, gamma_alpha=1.0, sites=1000, branch_mean=0.02),
+    "C1": dict(tips=64, model_kind=0, categories=1, gamma_alpha=1.0, sites=1000, branch_mean=0.02,
+               sim=SIM_REFERENCE),
     "C2": dict(tips=512, model_kind=1, categories=4, gamma_alpha=0.5, sites=20000, branch_mean=0.01,
-               gap_fraction=0.02),
+               gap_fraction=0.02, sim=SIM_REFERENCE),
     "C3": dict(tips=2048, model_kind=2, categories=4, gamma_alpha=0.5, sites=1000000, clock=1, dt_mean=5.0,
                rate_scale=1e-3, rate_sd=0.3),
     "C4": dict(tips=1000, model_kind=3, categories=4, gamma_alpha=0.5, sites=200000, branch_mean=0.05),
@@ -90,9 +157,9 @@ class Instance:
 
 
 def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int | None = None,
-             threads: int = 0) -> Instance:
+             threads: int = 0, sim: int | None = None) -> Instance:
     cfg = dict(CONFIGS[name])
-    spec = _L.SynthSpec()
+    spec = Spec()
     spec.tips = tips or cfg["tips"]
     spec.model_kind = cfg["model_kind"]
     spec.categories = cfg["categories"]
@@ -106,11 +173,12 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
     spec.gap_fraction = cfg.get("gap_fraction", 0.0)
     spec.seed = seed
     spec.threads = threads
+    spec.sim = cfg.get("sim", SIM_BLOCKED) if sim is None else sim
     L = lib()
     h = C.c_void_p()
     P = C.c_int()
     m = C.c_int()
-    check(L.pg_synth_create(C.byref(spec), C.byref(h), C.byref(P), C.byref(m)))
+    check(L.pgw_create(C.byref(spec), C.byref(h), C.byref(P), C.byref(m)))
     try:
         N = spec.tips
         n = 2 * N - 1
@@ -120,7 +188,7 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
         blen = np.zeros(n - 1)
         dt = np.zeros(n - 1)
         rr = np.zeros(n - 1)
-        check(L.pg_synth_tree(h, ptr(parent, C.c_int32), ptr(children, C.c_int32), ptr(post, C.c_int32),
+        check(L.pgw_tree(h, ptr(parent, C.c_int32), ptr(children, C.c_int32), ptr(post, C.c_int32),
                               ptr(blen, C.c_double), ptr(dt, C.c_double), ptr(rr, C.c_double)))
         mm = m.value
         q = np.zeros(mm * mm)
@@ -128,15 +196,31 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
         rev = C.c_int()
         cr = np.zeros(spec.categories)
         cp = np.zeros(spec.categories)
-        check(L.pg_synth_model(h, ptr(q, C.c_double), ptr(pi, C.c_double), C.byref(rev), ptr(cr, C.c_double),
+        check(L.pgw_model(h, ptr(q, C.c_double), ptr(pi, C.c_double), C.byref(rev), ptr(cr, C.c_double),
                                ptr(cp, C.c_double)))
         codes = np.zeros((N, P.value), np.int8)
         w = np.zeros(P.value, np.int64)
-        check(L.pg_synth_patterns(h, ptr(codes, C.c_int8), ptr(w, C.c_int64)))
+        check(L.pgw_patterns(h, ptr(codes, C.c_int8), ptr(w, C.c_int64)))
     finally:
-        L.pg_synth_free(h)
+        L.pgw_free(h)
     return Instance(name, N, parent, children.reshape(n + 1, 2), post, blen, dt, rr, q.reshape(mm, mm), pi,
                     bool(rev.value), cr, cp, codes, w, bool(spec.clock))
+
+
+def instance_digest(inst: Instance) -> str:
+    """sha256 over every input array of an evaluation (tree, patterns, model,
+    categories, lengths, durations): equal digests mean identical inputs.
+    Full-size parity fixtures (tests/golden/full_*.npz) record it."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in (inst.parent, inst.children, inst.post_order, inst.branch_lengths, inst.durations, inst.q, inst.pi,
+              inst.cat_rates, inst.cat_probs, inst.codes, inst.weights):
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
 
 
 def tips_of(cfg) -> int:
@@ -173,9 +257,29 @@ def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: i
     return inst
 
 
-def engine_for(inst: Instance, options=None):
-    """Builds a LikelihoodEngine over an Instance (tips bound in order)."""
-    from .api import LikelihoodEngine, RateCategories, SitePatternAlignment, SubstitutionModel, Tree
+def simulate_states(tip_count, parent, post_order, q, pi, reversible, cat_rates, cat_probs, branch_lengths,
+                    sites, seed):
+    """alignment.hpp:243-286 in the reference's draw order (one
+    mt19937_64(seed) stream): tip states [tip_count][sites] int8."""
+    m = int(np.asarray(q).shape[0])
+    out = np.zeros((tip_count, sites), np.int8)
+    q = np.ascontiguousarray(q, np.float64)
+    pi = np.ascontiguousarray(pi, np.float64)
+    cr = np.ascontiguousarray(cat_rates, np.float64)
+    cp = np.ascontiguousarray(cat_probs, np.float64)
+    b = np.ascontiguousarray(branch_lengths, np.float64)
+    par = np.ascontiguousarray(parent, np.int32)
+    post = np.ascontiguousarray(post_order, np.int32)
+    check(lib().pgw_simulate_states(tip_count, ptr(par, C.c_int32), ptr(post, C.c_int32), m, ptr(q, C.c_double),
+                                    ptr(pi, C.c_double), int(bool(reversible)), len(cr), ptr(cr, C.c_double),
+                                    ptr(cp, C.c_double), ptr(b, C.c_double), sites, seed, ptr(out, C.c_int8)))
+    return out
+
+
+def api_objects(inst: Instance):
+    """The product API's setup objects (Tree, SitePatternAlignment,
+    SubstitutionModel, RateCategories) for an Instance (tips bound in order)."""
+    from paper_1905_12146_b200.api import RateCategories, SitePatternAlignment, SubstitutionModel, Tree
 
     labels = inst.labels()
     tree = Tree(inst.tip_count, inst.parent, inst.children,
@@ -183,7 +287,14 @@ def engine_for(inst: Instance, options=None):
     aln = SitePatternAlignment(labels[1:inst.tip_count + 1], inst.states, inst.codes, inst.weights)
     model = SubstitutionModel(inst.q, inst.pi, inst.reversible)
     cats = RateCategories(inst.cat_rates, inst.cat_probs)
-    eng = LikelihoodEngine(tree, aln, model, cats, options)
+    return tree, aln, model, cats
+
+
+def engine_for(inst: Instance, options=None):
+    """Builds a LikelihoodEngine over an Instance (tips bound in order)."""
+    from paper_1905_12146_b200.api import LikelihoodEngine
+
+    eng = LikelihoodEngine(*api_objects(inst), options)
     if inst.clock:
         eng.set_clock_durations(inst.durations)
     return eng
