@@ -31,6 +31,7 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
 }
 int pg_walk4_nc(int nc);
+void* pg_walk4x_kernel(bool homog, bool hess, int nc, int L, size_t* smem);
 void* pg_walkm_kernel(int mp, bool hess);
 size_t pg_walkm_smem(int mp);
 int pg_walkm_wpc(int mp);
@@ -131,6 +132,7 @@ struct pg_engine {
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
+  bool use_walk4x = false;  // category-parallel 4-state walk (pg_walk4x.cuh): one CTA of L warps per tile
   bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
   int codes_mp = 0;        // MP the device tip codes' class columns are encoded for
   int walkm_wpc = 4;       // warps per CTA in walkm
@@ -569,20 +571,31 @@ struct pg_engine {
       G = L / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);
       const size_t tcb = size_t(L) * NC * 4;
-      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
-                  sizeof(double2);
+      // category-parallel variant: warp l of a CTA holds category l of a
+      // 32-pattern tile (PG_WALK4X=0 keeps the per-warp walk4 for A/B runs)
+      const char* wx = std::getenv("PG_WALK4X");
+      use_walk4x = (wx == nullptr || std::atoi(wx) != 0) &&
+                   pg_walk4x_kernel(branch_q.empty(), false, NC, L, &walk_smem) != nullptr;
+      if (use_walk4x) {
+        G = 1;
+        ntiles = (P + 31) / 32;
+      } else {
+        walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
+                    sizeof(double2);
+      }
     }
     if (use_walkm) {
-      use_walk4 = false;
+      use_walk4 = use_walk4x = false;
       LC = 1;
       G = 4;  // a quad of lanes per pattern (DMMA fragment layout)
       walkm_wpc = pg_walkm_wpc(MP);
       ntiles = (P + 8 * walkm_wpc - 1) / (8 * walkm_wpc);  // CTA tiles of 8 patterns per warp
       walk_smem = pg_walkm_smem(MP);
     }
-    const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : pgk::kWarpsPerBlock);
-    // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents
-    const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : size_t(32) * LC * MP;
+    const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : use_walk4x ? 1 : pgk::kWarpsPerBlock);
+    // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents;
+    // walk4x: one CTA tile's slot (L categories x 32 patterns x 4 states)
+    const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : use_walk4x ? size_t(L) * 32 * 4 : size_t(32) * LC * MP;
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
     // The grid (and with it the fixed-order reduction over warp rows) must
     // not depend on the run-time memory state, or results would not be
@@ -600,6 +613,8 @@ struct pg_engine {
       // CTA tiles: 4 warps per tile
       int ctas = std::max(1, std::min({maxw / walkm_wpc, std::max(ntiles, 1), std::max(cap / walkm_wpc, 1)}));
       TW = ctas * walkm_wpc;
+    } else if (use_walk4x) {
+      TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));  // CTAs (one accumulator row each)
     } else {
       TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
       TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
@@ -781,8 +796,11 @@ struct pg_engine {
 
   void evaluate(int flags, double* ll_out, double* g_out, double* h_out_) {
     if (!shards.empty()) {
-      group_evaluate(flags);
-    } else if (!begin_evaluate(flags)) {
+      group_evaluate(flags);  // every shard caches the reduced result
+      shards[0]->copy_out(flags, ll_out, g_out, h_out_);
+      return;
+    }
+    if (!begin_evaluate(flags)) {
       enqueue(flags, nullptr);
       PG_CUDA(cudaMemcpyAsync(h_out, d_out.p, size_t(out_width(flags, B())) * sizeof(double), cudaMemcpyDeviceToHost,
                               stream));
@@ -835,6 +853,17 @@ int pg_engine::walk_max_blocks_per_sm() {
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * walkm_wpc, walk_smem));
       nb = h == 0 ? b : std::min(nb, b);
+    }
+    return std::max(nb, 1);
+  }
+  if (use_walk4x) {
+    for (int v = 0; v < 2; ++v) {
+      size_t sm = 0;
+      const void* fn = pg_walk4x_kernel(branch_q.empty(), v & 1, NC, L, &sm);
+      PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      int b = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * L, sm));
+      nb = v == 0 ? b : std::min(nb, b);
     }
     return std::max(nb, 1);
   }
@@ -939,6 +968,13 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     for (int i = 0; i < 4; ++i) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
+    }
+    if (use_walk4x) {
+      size_t sm = 0;
+      void* fx = pg_walk4x_kernel(branch_q.empty(), do_hess, NC, L, &sm);
+      void* args[] = {&p4};
+      PG_CUDA(cudaLaunchKernel(fx, dim3(unsigned(TW)), dim3(32 * L), args, sm, stream));
+      return;
     }
     void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv, L);
     void* args[] = {&p4};
@@ -1455,7 +1491,7 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
 
 int pg_engine_variant(const pg_engine* e) {
   e = primary(e);
-  return e->use_walkm ? 2 : e->use_walk4 ? 1 : 0;
+  return e->use_walkm ? 2 : e->use_walk4x ? 3 : e->use_walk4 ? 1 : 0;
 }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {

@@ -115,3 +115,41 @@ def test_facade_config_scale_matches_oracle(tmp_path, name, sites, devargs, shar
                 v -= r_[c - 1] * g[c - 1]
             want[k] = v
         assert_vec(res["node_time"], want, what="node-time gradient")
+
+
+def build_adapter_exe(tmpdir):
+    exe = os.path.join(str(tmpdir), "adapter_test")
+    libdir = os.path.join(ROOT, "paper_1905_12146_b200", "_build")
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "adapter_test.cpp"), "-L", libdir, "-lphylograd_b200",
+                           f"-Wl,-rpath,{libdir}", "-o", exe])
+    return exe
+
+
+def test_reference_adapter_compiles(tmp_path):
+    """include/phylograd_b200/reference_adapter.hpp against stand-ins with the
+    reference types' member names (no Eigen in this image)."""
+    assert os.path.exists(build_adapter_exe(tmp_path))
+
+
+@pytest.mark.gpu
+def test_reference_adapter_runs_full_c2(tmp_path):
+    """make_engine(tree, alignment, model, categories) over reference-shaped
+    objects (dense tip partials, taxa in a different order than the tips) at
+    full C2 size equals the oracle."""
+    from tests.helpers import assert_logl, assert_vec, oracle_for
+    from workloads import synth
+
+    exe = build_adapter_exe(tmp_path)
+    inst = synth.generate("C2", seed=12146)
+    inp, out = os.path.join(str(tmp_path), "in.bin"), os.path.join(str(tmp_path), "out.bin")
+    write_instance(inp, inst)
+    r = subprocess.run([exe, inp, out], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    import numpy as np
+
+    d = np.fromfile(out, np.float64, count=1 + inst.branches)
+    ll, g, _ = oracle_for(inst, blocks=os.cpu_count() or 1).branch_gradient(False)
+    assert_logl(d[0], ll)
+    assert_vec(d[1:], g)

@@ -1,9 +1,11 @@
-"""Direct oracle parity of every walk4_kernel<HOMOG, HESS, NC, LCV> variant
-(the C2/C3 bench kernel): pattern counts large enough that the engine picks
-walk4, one lane per pattern (LCV=4, the C3 geometry) and two (LCV=2, the C2
-geometry) forced through PG_WALK4_LCV, homogeneous and per-branch
-generators, with and without the Hessian, gaps only (NC=5) and IUPAC
-ambiguity classes (NC=16)."""
+"""Direct oracle parity of every 4-state walk variant (the C2/C3 bench
+kernels): the category-parallel walk4x_kernel<HOMOG, HESS, NC, L> (default
+for 4 categories: warp l of a CTA holds category l of a 32-pattern tile) and
+the per-warp walk4_kernel<HOMOG, HESS, NC, LCV> with one lane per pattern
+(LCV=4) or two (LCV=2) forced through PG_WALK4X=0 / PG_WALK4_LCV;
+homogeneous and per-branch generators, with and without the Hessian, gaps
+only (NC=5) and IUPAC ambiguity classes (NC=16).  walk4x evaluates walk4's
+arithmetic chains in the same order, so the two agree bit for bit."""
 import numpy as np
 import pytest
 
@@ -18,10 +20,15 @@ from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCate
                                        SitePatternAlignment, SubstitutionModel, Tree, parse_fasta, parse_newick)
 
 
-@pytest.fixture(params=[4, 2], ids=["lcv4", "lcv2"])
+@pytest.fixture(params=["cat", 4, 2], ids=["walk4x", "lcv4", "lcv2"])
 def lcv(request, monkeypatch):
+    """The kernel variant under test; returns (kernel name, lanes per pattern)."""
+    if request.param == "cat":
+        monkeypatch.delenv("PG_WALK4X", raising=False)
+        return "walk4x_kernel", 1
+    monkeypatch.setenv("PG_WALK4X", "0")
     monkeypatch.setenv("PG_WALK4_LCV", str(request.param))
-    return request.param
+    return "walk4_kernel", 4 // request.param
 
 
 def _branch_q(seed, B, k=5):
@@ -63,8 +70,8 @@ def test_walk4_variants_c3_shape(lcv, homog, hess):
     eng, ref = _instance_pair(inst, bq)
     ll, g, h = ref.branch_gradient(hess)
     rep = eng.branch_gradient(hess)
-    assert eng.info()["kernel"] == "walk4_kernel"
-    assert eng.info()["lanes_per_pattern"] == 4 // lcv
+    assert eng.info()["kernel"] == lcv[0]
+    assert eng.info()["lanes_per_pattern"] == lcv[1]
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
     if hess:
@@ -76,7 +83,7 @@ def test_walk4_gaps_c2_shape(lcv):
     eng, ref = _instance_pair(inst)
     ll, g, _ = ref.branch_gradient(False)
     rep = eng.branch_gradient()
-    assert eng.info()["kernel"] == "walk4_kernel"
+    assert eng.info()["kernel"] == lcv[0]
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
 
@@ -104,7 +111,7 @@ def test_walk4_iupac_classes(lcv):
                    list(cats.rates), list(cats.probs), blocks=8)
     ll, g, h = ref.branch_gradient(True)
     rep = eng.branch_gradient(True)
-    assert eng.info()["kernel"] == "walk4_kernel"
+    assert eng.info()["kernel"] == lcv[0]
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
     assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
@@ -155,3 +162,23 @@ def test_walk4_other_category_counts(L, homog):
         assert_vec(rep.branch_gradient, g)
         if hess:
             assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+
+
+@pytest.mark.parametrize("name,sites,hess", [("C3", 40000, False), ("C3", 40000, True), ("C2", 12000, False)])
+def test_walk4x_bit_identical_to_walk4(monkeypatch, name, sites, hess):
+    """walk4x (category-parallel) and walk4 (one lane per pattern) evaluate
+    the same arithmetic chains: logL, gradient and Hessian agree bit for bit."""
+    inst = synth.generate(name, sites=sites, tips=256)
+    monkeypatch.setenv("PG_WALK4_LCV", "4")
+    monkeypatch.setenv("PG_WALK4X", "0")
+    e4, _ = _instance_pair(inst)
+    r4 = e4.branch_gradient(hess)
+    assert e4.info()["kernel"] == "walk4_kernel"
+    monkeypatch.delenv("PG_WALK4X")
+    ex, _ = _instance_pair(inst)
+    rx = ex.branch_gradient(hess)
+    assert ex.info()["kernel"] == "walk4x_kernel"
+    assert rx.log_likelihood == r4.log_likelihood
+    assert np.array_equal(rx.branch_gradient, r4.branch_gradient)
+    if hess:
+        assert np.array_equal(rx.hessian_diagonal, r4.hessian_diagonal)
