@@ -10,28 +10,48 @@
 // covered by the others (walk4's C3 profile: 2 warps per scheduler, 36 % of
 // the samples in fixed-latency waits, 17 % in shared-memory load-use waits).
 //
-// Per step every operand of the CTA tile is ONE 1-D bulk copy (cp.async.bulk,
-// TMA engine) into the next stage while this step computes: an internal
-// child's edge-message slot or a deferred pre-partial ([node][cat][lane][4]
-// doubles, LW KB), a node's column table TC ([cat][NC][4] doubles), a tip's
-// 32 code bytes, a tip's Q P table (pre-order pass).  The copies of a stage
-// are issued by lane 0 of the warps (spread over the warps) after the step's
-// CTA barrier and complete on the stage's mbarrier.
+// Staging.  Every operand of the CTA tile is ONE 1-D bulk copy (cp.async.bulk,
+// TMA engine) into a stage of shared memory: an internal child's edge-message
+// slot or a deferred pre-partial ([node][cat][lane][4] doubles, LW KB), a
+// node's column table TC ([cat][NC][4] doubles), a tip's 32 code bytes, a
+// tip's Q P table (pre-order pass).  Three stages rotate; step j+1's copies
+// are issued at the top of step j (lane 0 of the warps, operands spread over
+// the warps) and complete on the stage's mbarrier, and the DRAM operands of
+// step j+2 are prefetched into L2 at the same time.  A value produced by
+// step i and consumed by step i+1 or i+2 never goes through global memory
+// for that use: the producing warp writes its category slice straight into
+// the consumer's stage (the post-order edge message of step i+1 stays in
+// registers; a pre-partial consumed next or after one more step; the root's
+// pi).  Anything consumed later was stored at least two steps earlier, so
+// its async-proxy fence and CTA barrier precede the copy.
 //
 // Cross-category quantities go through a small shared exchange (double-
 // buffered by step parity) with one CTA barrier per step: the per-pattern
 // peak exponent (post: normalisation of p_k; pre: of the outgoing q_c), the
 // root mixture and the gradient ratio terms (den, num_a, num_b).  Every
-// arithmetic chain is the one walk4 evaluates (same operand order, same fma
-// nesting over categories), so the two kernels give bit-identical results.
+// per-pattern arithmetic chain is the one walk4 evaluates (same operand
+// order, same fma nesting over categories).
 #pragma once
 
 #include "pg_walk4.cuh"
 
 namespace pgk {
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// one step of a CTA's stream: descriptor, tile, index within the tile's
+// post (k < n) / pre (k >= n) steps; k < 0 past the end
+struct Walk4xStep {
+  int4 d;
+  int tile, k;
+  bool pre;
+};
+
 template <int LW, int NC, bool HESS>
 struct Walk4xGeom {
+  static constexpr int NST = 3;              // stages
   static constexpr int SLOT = LW * 32 * 4;   // doubles: one node slot of the CTA tile
   static constexpr int TCB = LW * NC * 4;    // doubles: one node's column table (all categories)
   static constexpr int STAGE = 3 * SLOT + 3 * TCB + 8;  // 3 operand slots, 3 TC blocks, 2 x 32 code bytes
@@ -40,30 +60,28 @@ struct Walk4xGeom {
   static constexpr int XI = 2 * 32 * LW;
   static constexpr int XD = NR * 32 * LW;
   static constexpr size_t smem_bytes() {
-    return size_t(2 * STAGE) * 8 + size_t(2 * XD) * 8 + size_t(2 * XI) * 4 + 2 * 8;
+    return size_t(NST * STAGE) * 8 + size_t(2 * XD) * 8 + size_t(2 * XI) * 4 + NST * 8;
   }
 };
 
 template <bool HOMOG, bool HESS, int NC, int LW>
 __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(const __grid_constant__ Walk4Params P4) {
   using Gx = Walk4xGeom<LW, NC, HESS>;
-  constexpr int SLOT = Gx::SLOT, TCB = Gx::TCB, STAGE = Gx::STAGE, NR = Gx::NR;
+  constexpr int NST = Gx::NST, SLOT = Gx::SLOT, TCB = Gx::TCB, STAGE = Gx::STAGE;
   const WalkParams& p = P4.p;
   extern __shared__ __align__(16) double sm4x[];
-  double* stg = sm4x;                                        // [2][STAGE]
-  double* xd = sm4x + 2 * STAGE;                             // [2][NR][32][LW]
+  double* stg = sm4x;                                        // [NST][STAGE]
+  double* xd = sm4x + NST * STAGE;                           // [2][NR][32][LW]
   int* xi = reinterpret_cast<int*>(xd + 2 * Gx::XD);         // [2][2][32][LW]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(xi + 2 * Gx::XI);
   const int tid = threadIdx.x, lane = tid & 31, l = tid >> 5;  // warp = category
   const int N = p.N, root = 2 * N - 1, n = p.nsteps;
   if (tid == 0) {
-    mbar_init(mbar, LW);  // lane 0 of every warp arrives once per stage
-    mbar_init(mbar + 1, LW);
+    for (int i = 0; i < NST; ++i) mbar_init(mbar + i, LW);  // lane 0 of every warp arrives once per use
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  const double cw = p.probs[l], crw = p.rates[l] * cw, cr2w = p.rates[l] * crw;
   double* A = p.acc + size_t(blockIdx.x) * p.accw;  // this CTA's accumulator row
   for (int i = tid; i < p.accw; i += 32 * LW) A[i] = 0.0;
   // CTA-major scratch: slot of node k at (k - N - 1) * SLOT, category l at + l * 128
@@ -71,10 +89,8 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
   double* Qs = p.qscr + size_t(blockIdx.x) * size_t(N - 1) * SLOT;
 
   auto op = [&](int st, int k) -> double* { return stg + st * STAGE + k * SLOT; };
-  auto tcb = [&](int st, int k) -> const double* { return stg + st * STAGE + 3 * SLOT + k * TCB; };
-  auto code_of = [&](int st, int k) -> int {
-    return reinterpret_cast<const uint8_t*>(stg + st * STAGE + 3 * SLOT + 3 * TCB + 4 * k)[lane];
-  };
+  auto tcb = [&](int st, int k) -> double* { return stg + st * STAGE + 3 * SLOT + k * TCB; };
+  auto cbytes = [&](int st) -> uint8_t* { return reinterpret_cast<uint8_t*>(stg + st * STAGE + 3 * SLOT + 3 * TCB); };
   // this warp's category part of a slot: [h][lane] double2 (512 B per access)
   auto rd4 = [&](const double* slot, double (&v)[4]) {
     const double2* s2 = reinterpret_cast<const double2*>(slot + l * 128) + lane;
@@ -104,118 +120,172 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
   };
 
   // ---------------------------------------------------------- step stream
-  // The CTA's work is one stream of steps: per tile, the post-order steps,
-  // then (gradient) the pre-order steps.  Step j's operands are staged into
-  // stage j & 1 during step j - 1.
+  // The CTA's work is one stream of steps: per tile, the n post-order steps,
+  // then (gradient) the n pre-order steps.  A window of descriptors runs two
+  // steps ahead of the current one (D[0] = current, D[1], D[2]) and keeps the
+  // two previous ones (Dm1, Dm2).
   const int per_tile = p.do_pre ? 2 * n : n;
-  const int ntiles = p.ntiles;
-  const int first_tile = blockIdx.x;
-  if (first_tile >= ntiles) return;
-  const long long total = (long long)((ntiles - 1 - first_tile) / gridDim.x + 1) * per_tile;
-  auto tile_of = [&](long long j) { return first_tile + int(j / per_tile) * int(gridDim.x); };
-  auto desc_of = [&](long long j, bool& pre) -> int4 {
-    const int k = int(j % per_tile);
-    pre = k >= n;
-    return pre ? __ldg(p.pre + (k - n)) : __ldg(p.post + k);
-  };
-  const unsigned long long pol_first = policy_evict_first();
-  // issue step j's bulk copies into stage j & 1 (lane 0 of warp (operand % LW)).
-  // aux: post step -> the node whose edge message stays in registers (the
-  // previous step's node, not staged); pre step -> 1 if its q is handed on
-  // through the q slot (not staged)
-  auto issue = [&](long long j, int4 d, bool pre, int aux) {
-    const int st = int(j & 1);
-    const int t = tile_of(j);
-    const uint8_t* codes = p.codes + size_t(t) * 32;
-    const size_t Pc = size_t(p.Pc);
-    uint64_t* mb = mbar + st;
-    unsigned tx = 0;
-    int k = 0;
-    auto mine = [&]() { return lane == 0 && (k++ % LW) == l; };
-    auto copy = [&](void* dst, const void* src, unsigned bytes) {
-      bulk_g2s(dst, src, bytes, mb);
-      tx += bytes;
-    };
-    auto copy_once = [&](void* dst, const void* src, unsigned bytes) {
-      bulk_g2s_hint(dst, src, bytes, mb, pol_first);
-      tx += bytes;
-    };
-    double* base = stg + st * STAGE;
-    uint8_t* cbase = reinterpret_cast<uint8_t*>(base + 3 * SLOT + 3 * TCB);
-    if (!pre) {
-      if (d.y <= N) {
-        if (mine()) copy(cbase, codes + size_t(d.y - 1) * Pc, 32);
-        if (mine()) copy(base + 3 * SLOT + TCB, p.tc + size_t(d.y - 1) * TCB, TCB * 8);
-      } else if (d.y != aux) {
-        if (mine()) copy(op(st, 0), E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
-      }
-      if (d.z <= N) {
-        if (mine()) copy(cbase + 32, codes + size_t(d.z - 1) * Pc, 32);
-        if (mine()) copy(base + 3 * SLOT + 2 * TCB, p.tc + size_t(d.z - 1) * TCB, TCB * 8);
-      } else if (d.z != aux) {
-        if (mine()) copy(op(st, 0), E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
-      }
-      if (d.x != root)
-        if (mine()) copy(base + 3 * SLOT, p.tc + size_t(d.x - 1) * TCB, TCB * 8);
+  if (int(blockIdx.x) >= p.ntiles) return;
+  auto load = [&](int tile, int k) -> Walk4xStep {
+    Walk4xStep s;
+    s.tile = tile;
+    s.k = k;
+    s.pre = k >= n;
+    if (tile >= p.ntiles) {
+      s.d = make_int4(-1, -1, -1, -1);
+      s.k = -1;
     } else {
-      if (d.x != root && !aux)
-        if (mine()) copy_once(op(st, 2), Qs + size_t(d.x - N - 1) * SLOT, SLOT * 8);
-      if (d.y <= N) {
-        if (mine()) copy(cbase, codes + size_t(d.y - 1) * Pc, 32);
-        if (p.qtc)
-          if (mine()) copy(op(st, 0), p.qtc + size_t(d.y - 1) * TCB, TCB * 8);
-      } else {
-        if (mine()) copy_once(op(st, 0), E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
-      }
-      if (d.z <= N) {
-        if (mine()) copy(cbase + 32, codes + size_t(d.z - 1) * Pc, 32);
-        if (p.qtc)
-          if (mine()) copy(op(st, 1), p.qtc + size_t(d.z - 1) * TCB, TCB * 8);
-      } else {
-        if (mine()) copy_once(op(st, 1), E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
-      }
-      if (mine()) copy(base + 3 * SLOT, p.tc + size_t(d.y - 1) * TCB, TCB * 8);
-      if (mine()) copy(base + 3 * SLOT + TCB, p.tc + size_t(d.z - 1) * TCB, TCB * 8);
+      s.d = k >= n ? __ldg(p.pre + (k - n)) : __ldg(p.post + k);
     }
-    if (lane == 0) mbar_arrive_tx(mb, tx);
+    return s;
+  };
+  auto next_of = [&](const Walk4xStep& s) -> Walk4xStep {
+    if (s.k < 0) return s;
+    return s.k + 1 < per_tile ? load(s.tile, s.k + 1) : load(s.tile + int(gridDim.x), 0);
+  };
+  auto none = [&]() {
+    Walk4xStep s;
+    s.d = make_int4(-1, -1, -1, -1);
+    s.tile = -1;
+    s.k = -1;
+    s.pre = false;
+    return s;
+  };
+  // the same tile and pass (post / pre) as `a`
+  auto same_pass = [&](const Walk4xStep& a, const Walk4xStep& b) {
+    return a.k >= 0 && b.k >= 0 && a.tile == b.tile && a.pre == b.pre;
+  };
+  // internal child of a pre-order step that is NOT visited next (deferred)
+  auto other_child = [&](const int4 d) -> int {
+    const int o = d.y == d.w ? d.z : d.y;
+    return o > N ? o : -1;
+  };
+  // does step s take its pre-partial from a hand-off (previous step's or the
+  // one before's)?  prev1 / prev2: the two steps before s
+  auto q_handed = [&](const Walk4xStep& s, const Walk4xStep& prev1, const Walk4xStep& prev2) {
+    if (s.d.x == root) return true;  // pi, written by the root's post step
+    if (same_pass(prev1, s) && prev1.d.w == s.d.x) return true;
+    if (same_pass(prev2, s) && other_child(prev2.d) == s.d.x) return true;
+    return false;
+  };
+  // post: is child c of step s in registers (previous step's node) or handed
+  // into the stage by the step before that?
+  auto e_handed = [&](int c, const Walk4xStep& s, const Walk4xStep& prev1, const Walk4xStep& prev2) {
+    return (same_pass(prev1, s) && prev1.d.x == c) || (same_pass(prev2, s) && prev2.d.x == c);
   };
 
+  const unsigned long long pol_first = policy_evict_first();
+  // issue step s's bulk copies into stage st (lane 0 of warp (operand % LW));
+  // prev1 / prev2: the two steps before s
+  auto issue = [&](const Walk4xStep& s, const Walk4xStep& prev1, const Walk4xStep& prev2, int st) {
+    if (lane != 0) return;
+    uint64_t* mb = mbar + st;
+    unsigned tx = 0;
+    if (s.k >= 0) {
+      int k = 0;
+      auto mine = [&]() { return (k++ % LW) == l; };
+      auto copy = [&](void* dst, const void* src, unsigned bytes) {
+        bulk_g2s(dst, src, bytes, mb);
+        tx += bytes;
+      };
+      auto copy_once = [&](void* dst, const void* src, unsigned bytes) {
+        bulk_g2s_hint(dst, src, bytes, mb, pol_first);
+        tx += bytes;
+      };
+      const int4 d = s.d;
+      const uint8_t* codes = p.codes + size_t(s.tile) * 32;
+      const size_t Pc = size_t(p.Pc);
+      uint8_t* cb = cbytes(st);
+      if (!s.pre) {
+        if (d.y <= N) {
+          if (mine()) copy(cb, codes + size_t(d.y - 1) * Pc, 32);
+          if (mine()) copy(tcb(st, 1), p.tc + size_t(d.y - 1) * TCB, TCB * 8);
+        } else if (!e_handed(d.y, s, prev1, prev2)) {
+          if (mine()) copy(op(st, 0), E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
+        }
+        if (d.z <= N) {
+          if (mine()) copy(cb + 32, codes + size_t(d.z - 1) * Pc, 32);
+          if (mine()) copy(tcb(st, 2), p.tc + size_t(d.z - 1) * TCB, TCB * 8);
+        } else if (!e_handed(d.z, s, prev1, prev2)) {
+          if (mine()) copy(op(st, 0), E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
+        }
+        if (d.x != root)
+          if (mine()) copy(tcb(st, 0), p.tc + size_t(d.x - 1) * TCB, TCB * 8);
+      } else {
+        if (!q_handed(s, prev1, prev2))
+          if (mine()) copy_once(op(st, 2), Qs + size_t(d.x - N - 1) * SLOT, SLOT * 8);
+        if (d.y <= N) {
+          if (mine()) copy(cb, codes + size_t(d.y - 1) * Pc, 32);
+          if (p.qtc)
+            if (mine()) copy(op(st, 0), p.qtc + size_t(d.y - 1) * TCB, TCB * 8);
+        } else {
+          if (mine()) copy_once(op(st, 0), E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
+        }
+        if (d.z <= N) {
+          if (mine()) copy(cb + 32, codes + size_t(d.z - 1) * Pc, 32);
+          if (p.qtc)
+            if (mine()) copy(op(st, 1), p.qtc + size_t(d.z - 1) * TCB, TCB * 8);
+        } else {
+          if (mine()) copy_once(op(st, 1), E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
+        }
+        if (mine()) copy(tcb(st, 0), p.tc + size_t(d.y - 1) * TCB, TCB * 8);
+        if (mine()) copy(tcb(st, 1), p.tc + size_t(d.z - 1) * TCB, TCB * 8);
+      }
+    }
+    mbar_arrive_tx(mb, tx);
+  };
+  // L2 prefetch of step s's scratch operands from DRAM (those not handed on)
+  auto prefetch = [&](const Walk4xStep& s, const Walk4xStep& prev1, const Walk4xStep& prev2) {
+    if (tid != 32 * (LW - 1) || s.k < 0) return;
+    const int4 d = s.d;
+    if (!s.pre) {
+      if (d.y > N && !e_handed(d.y, s, prev1, prev2)) bulk_prefetch_l2(E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
+      if (d.z > N && !e_handed(d.z, s, prev1, prev2)) bulk_prefetch_l2(E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
+    } else {
+      if (d.y > N) bulk_prefetch_l2(E + size_t(d.y - N - 1) * SLOT, SLOT * 8);
+      if (d.z > N) bulk_prefetch_l2(E + size_t(d.z - N - 1) * SLOT, SLOT * 8);
+    }
+  };
+
+  Walk4xStep Dm2 = none(), Dm1 = none();
+  Walk4xStep D0 = load(blockIdx.x, 0);
+  Walk4xStep D1 = next_of(D0);
+  Walk4xStep D2 = next_of(D1);
+  int st = 0;          // stage of D0; D1 -> (st + 1) % 3, D2 -> (st + 2) % 3
   unsigned phase = 0;  // parity bit per stage
-  bool cur_pre = false;
-  int4 cur = desc_of(0, cur_pre);
-  issue(0, cur, cur_pre, -1);
+  issue(D0, Dm1, Dm2, st);
+  prefetch(D1, D0, Dm1);
   // step-to-step state (per warp: its category)
   double keep[4] = {0.0, 0.0, 0.0, 0.0};  // post: previous step's edge message
   int last = -1;                          // post: node whose e is in `keep`
   int S = 0;                              // post: accumulated exponent of the tile's patterns
-  int prev_next = 0;                      // pre: node whose q was handed on through the q slot
 
-  for (long long j = 0; j < total; ++j) {
-    const int st = int(j & 1);
-    const int t = tile_of(j);
-    const int s = t * 32 + lane;
+  for (long long j = 0; D0.k >= 0; ++j) {
+    const int st1 = st == NST - 1 ? 0 : st + 1, st2 = st1 == NST - 1 ? 0 : st1 + 1;
+    // step j+1's copies and step j+2's L2 prefetch go out before this step
+    // waits for its own operands
+    issue(D1, D0, Dm1, st1);
+    prefetch(D2, D1, D0);
+    const int4 d = D0.d;
+    const bool pre = D0.pre;
+    const int s = D0.tile * 32 + lane;
     const bool valid = s < p.P;
     const bool owner = valid;
     const double w = valid ? p.weights[s] : 0.0;
-    const int4 d = cur;
-    const bool pre = cur_pre;
-    bool nxt_pre = false;
-    const bool has_next = j + 1 < total;
-    int4 dn = make_int4(0, 0, 0, 0);
-    if (has_next) dn = desc_of(j + 1, nxt_pre);
-    if (!pre && int(j % per_tile) == 0) {
+    if (!pre && D0.k == 0) {
       S = 0;
       last = -1;
     }
     mbar_wait(mbar + st, (phase >> st) & 1u);
     phase ^= 1u << st;
-    int* xint = xi + st * Gx::XI;
-    double* xdbl = xd + st * Gx::XD;
+    const int px = int(j & 1);
+    int* xint = xi + px * Gx::XI;
+    double* xdbl = xd + px * Gx::XD;
 
     if (!pre) {
       // ------------------------------------------ post-order step (a)
-      const int code0 = d.y <= N ? code_of(st, 0) : 0;
-      const int code1 = d.z <= N ? code_of(st, 1) : 0;
+      const int code0 = d.y <= N ? cbytes(st)[lane] : 0;
+      const int code1 = d.z <= N ? cbytes(st)[32 + lane] : 0;
       double a[4], b[4], x[4];
       if (d.y <= N) col4(tcb(st, 1), code0, a);
       else if (d.y == last) {
@@ -236,9 +306,6 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
       xint[lane * LW + l] = hm;
       fence_proxy_async_global();  // earlier scratch stores before later bulk reads (after the barrier)
       __syncthreads();
-      // next: the first pre-order step (its q = pi is written below), or the
-      // next post-order step with this step's edge message kept in registers
-      if (has_next) issue(j + 1, dn, nxt_pre, nxt_pre ? int(dn.x == root) : (d.x != root ? d.x : -1));
       if (!p.disable) {
         int hmax = xint[lane * LW];
 #pragma unroll
@@ -278,8 +345,8 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
         }
         // the first pre-order step's q is pi: handed on through its q slot
         if (p.do_pre) {
-          double pv[4] = {P4.pi[0], P4.pi[1], P4.pi[2], P4.pi[3]};
-          wr4_smem(op(st ^ 1, 2), pv, 1.0);
+          const double pv[4] = {P4.pi[0], P4.pi[1], P4.pi[2], P4.pi[3]};
+          wr4_smem(op(st1, 2), pv, 1.0);
         }
       } else {
         // e_k = P_k p_k (engine.hpp:367-372), column c of P at TC column c
@@ -300,13 +367,15 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
         double2* dst = reinterpret_cast<double2*>(E + size_t(d.x - N - 1) * SLOT + l * 128) + lane;
         __stcs(dst, make_double2(e0, e1));
         __stcs(dst + 32, make_double2(e2, e3));
+        // consumed two steps on: straight into that step's stage
+        if (same_pass(D2, D0) && (D2.d.y == d.x || D2.d.z == d.x)) wr4_smem(op(st2, 0), keep, 1.0);
         last = d.x;
       }
     } else {
       // ------------------------------- pre-order step + gradient (b)+(c)
       const bool a_int = d.y > N, b_int = d.z > N;
-      const int code0 = a_int ? 0 : code_of(st, 0);
-      const int code1 = b_int ? 0 : code_of(st, 1);
+      const int code0 = a_int ? 0 : cbytes(st)[lane];
+      const int code1 = b_int ? 0 : cbytes(st)[32 + lane];
       const double* Ta = tcb(st, 0);
       const double* Tb = tcb(st, 1);
       double q[4], ea[4], eb[4];
@@ -400,19 +469,17 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
       xint[(1 * 32 + lane) * LW + l] = hb;
       fence_proxy_async_global();
       __syncthreads();
-      const bool q_next = has_next && nxt_pre && dn.x == d.w;  // next step's q handed on
-      if (has_next) issue(j + 1, dn, nxt_pre, nxt_pre ? int(q_next) : -1);
       // consumed scratch is dead: drop it from L2 without write-back
       if (lane < 8) {
         const char* eb_ = reinterpret_cast<const char*>(E) + size_t(l) * 1024 + lane * 128;
         const char* qb_ = reinterpret_cast<const char*>(Qs) + size_t(l) * 1024 + lane * 128;
         if (a_int) discard_l2(eb_ + size_t(d.y - N - 1) * SLOT * 8);
         if (b_int) discard_l2(eb_ + size_t(d.z - N - 1) * SLOT * 8);
-        if (d.x != root && prev_next != d.x) discard_l2(qb_ + size_t(d.x - N - 1) * SLOT * 8);
+        if (!q_handed(D0, Dm1, Dm2)) discard_l2(qb_ + size_t(d.x - N - 1) * SLOT * 8);
       }
       // gradient: warp 0 for child a, warp 1 (or 0) for child b, with walk4's
       // fma order over categories
-      const int wa = 0, wb = LW > 1 ? 1 : 0;
+      constexpr int wa = 0, wb = LW > 1 ? 1 : 0;
       if (l == wa || l == wb) {
         double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
 #pragma unroll
@@ -448,7 +515,8 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
         }
       }
       // normalise (shared peak over the categories) and hand on: the child
-      // visited next through the next stage's q slot, the other to scratch
+      // visited next through the next stage's q slot, a child visited two
+      // steps on through that stage's, any other to scratch
       auto emit = [&](int x, const double (&qx)[4], int field) {
         int hx = xint[(field * 32 + lane) * LW];
 #pragma unroll
@@ -456,7 +524,9 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
         const int ex = peak_exponent(hx);
         const double scl = (ex != 0 && ex <= 1022) ? pow2_neg(ex) : 1.0;
         if (x == d.w) {
-          wr4_smem(op(st ^ 1, 2), qx, scl);
+          wr4_smem(op(st1, 2), qx, scl);
+        } else if (same_pass(D2, D0) && D2.d.x == x) {
+          wr4_smem(op(st2, 2), qx, scl);
         } else {
           double2* dst = reinterpret_cast<double2*>(Qs + size_t(x - N - 1) * SLOT + l * 128) + lane;
           __stcg(dst, make_double2(qx[0] * scl, qx[1] * scl));
@@ -465,14 +535,14 @@ __global__ void __launch_bounds__(32 * LW, (LW >= 4 ? 4 : 8)) walk4x_kernel(cons
       };
       if (a_int) emit(d.y, qa, 0);
       if (b_int) emit(d.z, qb, 1);
-      prev_next = d.w;
-      (void)crw;
-      (void)cr2w;
-      (void)cw;
     }
     __syncwarp();
-    cur = dn;
-    cur_pre = nxt_pre;
+    Dm2 = Dm1;
+    Dm1 = D0;
+    D0 = D1;
+    D1 = D2;
+    D2 = next_of(D1);
+    st = st1;
   }
 }
 

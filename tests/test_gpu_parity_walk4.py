@@ -165,9 +165,11 @@ def test_walk4_other_category_counts(L, homog):
 
 
 @pytest.mark.parametrize("name,sites,hess", [("C3", 40000, False), ("C3", 40000, True), ("C2", 12000, False)])
-def test_walk4x_bit_identical_to_walk4(monkeypatch, name, sites, hess):
+def test_walk4x_matches_walk4(monkeypatch, name, sites, hess):
     """walk4x (category-parallel) and walk4 (one lane per pattern) evaluate
-    the same arithmetic chains: logL, gradient and Hessian agree bit for bit."""
+    the same per-pattern arithmetic chains; only the grouping of the
+    per-tile sums into accumulator rows differs (CTA rows vs warp rows), so
+    logL, gradient and Hessian agree to ~1e-13 relative."""
     inst = synth.generate(name, sites=sites, tips=256)
     monkeypatch.setenv("PG_WALK4_LCV", "4")
     monkeypatch.setenv("PG_WALK4X", "0")
@@ -178,7 +180,7 @@ def test_walk4x_bit_identical_to_walk4(monkeypatch, name, sites, hess):
     ex, _ = _instance_pair(inst)
     rx = ex.branch_gradient(hess)
     assert ex.info()["kernel"] == "walk4x_kernel"
-    assert rx.log_likelihood == r4.log_likelihood
-    assert np.array_equal(rx.branch_gradient, r4.branch_gradient)
+    assert_logl(rx.log_likelihood, r4.log_likelihood, rtol=1e-13)
+    assert_vec(rx.branch_gradient, r4.branch_gradient, rtol=1e-12)
     if hess:
-        assert np.array_equal(rx.hessian_diagonal, r4.hessian_diagonal)
+        assert_vec(rx.hessian_diagonal, r4.hessian_diagonal, rtol=1e-11, what="hessian")
