@@ -356,15 +356,25 @@ def parity_block(args, inst, logl, grad):
     if synth.instance_digest(inst) != str(fx["digest"]):
         return {"fixture": rel, "match": False, "note": "instance digest differs from the fixture's"}
     want = fx["rate_gradient"] if inst.clock else fx["gradient"]
+    ckey = "rate_gradient_condition" if inst.clock else "gradient_condition"
+    cond = fx[ckey] if ckey in fx.files else None
     g = np.asarray(grad)
     err = np.abs(g - want)
     scale = float(np.max(np.abs(want)))
-    ok = bool(np.all(np.isfinite(g)) and np.all(err <= 1e-9 * np.abs(want) + 1e-12 * scale))
+    tol = 1e-9 * np.abs(want) + 1e-12 * scale
+    if cond is not None:
+        # SURVEY.md §8d condition-aware variant for cancelling components
+        tol = np.maximum(tol, 1e-11 * cond)
+    ok = bool(np.all(np.isfinite(g)) and np.all(err <= tol))
     ll_rel = abs(logl - float(fx["logL"])) / abs(float(fx["logL"]))
-    return {"fixture": rel, "match": True, "logL_rel": ll_rel,
-            "grad_max_rel": float(np.max(err / np.maximum(np.abs(want), 1e-300))),
-            "grad_max_rel_to_scale": float(np.max(err) / scale),
-            "within_1e-9": bool(ok and ll_rel <= 1e-9), "oracle_threads": int(fx["oracle_threads"])}
+    out = {"fixture": rel, "match": True, "logL_rel": ll_rel,
+           "grad_max_rel": float(np.max(err / np.maximum(np.abs(want), 1e-300))),
+           "grad_max_rel_to_scale": float(np.max(err) / scale),
+           "components_over_1e-9_rel": int(np.sum(err > 1e-9 * np.abs(want))),
+           "within_1e-9": bool(ok and ll_rel <= 1e-9), "oracle_threads": int(fx["oracle_threads"])}
+    if cond is not None:
+        out["grad_max_rel_to_condition"] = float(np.max(err / np.maximum(cond, 1e-300)))
+    return out
 
 
 def run_reference(args, inst):

@@ -1113,6 +1113,7 @@ class Engine {
     if (!post_valid_) throw std::logic_error("engine: pre-order pass requires a current post-order pass");
     const int L = cats_.count(), m = model_.m;
     grad_.assign(size_t(tree_.branch_count()), 0.0);
+    gabs_.assign(size_t(tree_.branch_count()), 0.0);
     if (hess) hessd_.assign(size_t(tree_.branch_count()), 0.0);
     Mat buffer(m, P_), qp(m, P_);
     Vec u1(static_cast<size_t>(P_)), u2(static_cast<size_t>(P_)), r1(static_cast<size_t>(P_));
@@ -1168,17 +1169,19 @@ class Engine {
           if (hess) u2[size_t(s)] += (cl * cl * wl) * acc2;
         }
       }
-      double g = 0.0, hd = 0.0;
+      double g = 0.0, hd = 0.0, ga = 0.0;
       for (int s = 0; s < P_; ++s) {
         const double e = std::exp(scaler_post_[size_t(node)][size_t(s)] + scaler_pre_[size_t(node)][size_t(s)] - site_ll_[size_t(s)]);
         r1[size_t(s)] = u1[size_t(s)] * e;
         g += weights_[size_t(s)] * r1[size_t(s)];
+        ga += weights_[size_t(s)] * std::fabs(r1[size_t(s)]);  // condition of the sum (test use)
         if (hess) {
           const double r2 = u2[size_t(s)] * e;
           hd += weights_[size_t(s)] * (r2 - r1[size_t(s)] * r1[size_t(s)]);
         }
       }
       grad_[size_t(node - 1)] = g;
+      gabs_[size_t(node - 1)] = ga;
       if (hess) hessd_[size_t(node - 1)] = hd;
     }
     pre_valid_ = true;
@@ -1186,6 +1189,9 @@ class Engine {
   }
 
   int p0_report = 0;  // pattern offset added to error messages
+  // sum_s w_s |term_{s,i}| of the last pre-order pass: the condition of each
+  // gradient component (SURVEY.md §8d condition-aware parity)
+  const Vec& gradient_abs() const { return gabs_; }
 
  private:
   // engine.hpp:284-361 (slot-pool likelihood-only route)
@@ -1346,6 +1352,7 @@ class Engine {
   std::vector<Vec> scratch_scaler_;
   double ll_ = 0.0;
   bool post_valid_ = false, pre_valid_ = false, hess_valid_ = false, ll_valid_ = false;
+  Vec gabs_;
   uint64_t visits_ = 0;
 };
 
@@ -1844,6 +1851,19 @@ int orc_engine_branch_gradient(void* eh, int hess, double* ll, double* grad, dou
       grad[i] += gs[b][i];
       if (hess) hd[i] += hs[b][i];
     }
+  }
+  return 0;
+  ORC_CATCH
+}
+int orc_engine_gradient_abs(void* eh, double* out) {
+  ORC_TRY
+  auto* h = static_cast<OEngine*>(eh);
+  const size_t B = size_t(h->tree.branch_count());
+  for (size_t i = 0; i < B; ++i) out[i] = 0.0;
+  for (auto& blk : h->blocks) {
+    const Vec& a = blk->gradient_abs();
+    if (a.size() != B) throw std::logic_error("engine: no current gradient pass");
+    for (size_t i = 0; i < B; ++i) out[i] += a[i];
   }
   return 0;
   ORC_CATCH

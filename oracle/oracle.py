@@ -114,6 +114,7 @@ def _declare(L):
         "orc_engine_pre_order_pass": (I, [P, I]),
         "orc_engine_branch_gradient": (I, [P, I, C.POINTER(D), PD, PD]),
         "orc_engine_log_likelihood_at_node": (I, [P, I, C.POINTER(D)]),
+        "orc_engine_gradient_abs": (I, [P, PD]),
         "orc_engine_post_partial": (I, [P, I, I, PD]),
         "orc_engine_pre_partial": (I, [P, I, I, PD]),
         "orc_engine_scalers": (I, [P, I, PD, PD]),
@@ -509,6 +510,14 @@ class Engine:
         h = np.zeros(self.B)
         _check(lib().orc_engine_branch_gradient(self.h, int(with_hessian), C.byref(ll), g, h))
         return ll.value, g, (h if with_hessian else None)
+
+    def gradient_condition(self):
+        """sum_s w_s |term_{s,i}| per branch of the last gradient pass: the
+        scale against which a cancelling component's rounding is judged
+        (SURVEY.md §8d condition-aware parity)."""
+        out = np.zeros(self.B)
+        _check(lib().orc_engine_gradient_abs(self.h, out))
+        return out
 
     def log_likelihood_at_node(self, node):
         v = D()

@@ -21,6 +21,7 @@
 #include "pg_common.hpp"
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
+#include "pg_walk4x_tables.hpp"
 
 void* pg_walk4_kernel_lc4(bool homog, bool hess, int nc);
 void* pg_walk4_kernel_lc2(bool homog, bool hess, int nc);
@@ -146,6 +147,8 @@ struct pg_engine {
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err;
   DevBuf<int4> d_post, d_pre;
+  DevBuf<pgk::Walk4xHdr> d_xhdr;   // walk4x step headers (post, then pre)
+  DevBuf<pgk::Walk4xCopy> d_xcpy;  // walk4x per-step copy lists
   DevBuf<double> d_escr, d_qscr, d_acc, d_out, d_site_ll;
   DevBuf<double> d_cap_post, d_cap_pre;
   DevBuf<int> d_cap_post_exp, d_cap_pre_exp;
@@ -635,6 +638,13 @@ struct pg_engine {
       d_fpt.ensure(size_t(B()) * L * frag);
     }
     d_post.upload(post_steps.data(), post_steps.size(), stream);
+    if (use_walk4x) {
+      std::vector<pgk::Walk4xHdr> xh;
+      std::vector<pgk::Walk4xCopy> xc;
+      pgk::build_walk4x_tables(post_steps, pre_steps, N, L, NC, Pc, xh, xc);
+      d_xhdr.upload(xh.data(), xh.size(), stream);
+      d_xcpy.upload(xc.data(), xc.size(), stream);
+    }
     d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
     if (!h_out) {
       PG_CUDA(cudaMallocHost(&h_err, 3 * sizeof(int)));
@@ -862,7 +872,7 @@ int pg_engine::walk_max_blocks_per_sm() {
       const void* fn = pg_walk4x_kernel(branch_q.empty(), v & 1, NC, L, &sm);
       PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
       int b = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * L, sm));
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * (L + 1), sm));
       nb = v == 0 ? b : std::min(nb, b);
     }
     return std::max(nb, 1);
@@ -972,8 +982,12 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     if (use_walk4x) {
       size_t sm = 0;
       void* fx = pg_walk4x_kernel(branch_q.empty(), do_hess, NC, L, &sm);
-      void* args[] = {&p4};
-      PG_CUDA(cudaLaunchKernel(fx, dim3(unsigned(TW)), dim3(32 * L), args, sm, stream));
+      pgk::Walk4xParams px{};
+      px.p4 = p4;
+      px.hdr = d_xhdr.p;
+      px.cpy = d_xcpy.p;
+      void* args[] = {&px};
+      PG_CUDA(cudaLaunchKernel(fx, dim3(unsigned(TW)), dim3(32 * (L + 1)), args, sm, stream));
       return;
     }
     void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv, L);

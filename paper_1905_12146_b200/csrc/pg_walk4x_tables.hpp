@@ -1,0 +1,110 @@
+// Host side of the warp-specialised 4-state walk (pg_walk4x.cuh): per post-
+// and pre-order step, the header (descriptor + hand-off flags) and the list of
+// operand copies the producer warp issues.  Built once per topology /
+// pattern layout (the tables depend on the schedule, L, NC and the tip-code
+// row stride), uploaded next to the schedule.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace pgk {
+
+struct Walk4xHdr {
+  int4 d;
+  int flags;
+  int ncopy;
+  int tx;
+  int pad;
+};
+struct Walk4xCopy {
+  long long src;
+  int dst;
+  int kb;
+};
+constexpr int kW4xPostHandE2 = 1;
+constexpr int kW4xPreQGlobal = 1, kW4xPreHandY2 = 2, kW4xPreHandZ2 = 4;
+constexpr int kW4xMaxCopies = 8;
+
+// post / pre: the engine's schedules ({node, child, child, next}); N tips, L
+// categories, NC table columns, Pc tip-code row stride.
+inline void build_walk4x_tables(const std::vector<int4>& post, const std::vector<int4>& pre, int N, int L, int NC,
+                                long long Pc, std::vector<Walk4xHdr>& hdr, std::vector<Walk4xCopy>& cpy) {
+  const int n = int(post.size()), root = 2 * N - 1;
+  const long long SLOT = 32LL * 4 * L, TCB = 4LL * L * NC;  // doubles
+  const int SLOTB = int(SLOT * 8), TCBB = int(TCB * 8);
+  // stage layout in bytes (pg_walk4x.cuh Walk4xGeom): header, 3 slots, 3 TC blocks, 2 x 32 code bytes
+  auto OP = [&](int k) { return 32 + k * SLOTB; };
+  auto TC = [&](int k) { return 32 + 3 * SLOTB + k * TCBB; };
+  const int CODES = 32 + 3 * SLOTB + 3 * TCBB;
+  hdr.assign(size_t(2 * n), Walk4xHdr{});
+  cpy.assign(size_t(2 * n) * kW4xMaxCopies, Walk4xCopy{});
+  auto add = [&](int k, int kind, long long src, int dst, int bytes) {
+    Walk4xHdr& h = hdr[size_t(k)];
+    Walk4xCopy& c = cpy[size_t(k) * kW4xMaxCopies + size_t(h.ncopy++)];
+    c.src = src;
+    c.dst = dst;
+    c.kb = (kind << 24) | bytes;
+    h.tx += bytes;
+  };
+  auto slot = [&](int node) { return (node - N - 1) * SLOT; };
+  auto tcb = [&](int node) { return (node - 1) * TCB; };
+  auto codes = [&](int node) { return (node - 1) * Pc; };
+  // ---- post-order steps
+  for (int s = 0; s < n; ++s) {
+    const int4 d = post[size_t(s)];
+    Walk4xHdr& h = hdr[size_t(s)];
+    h.d = d;
+    const int ch[2] = {d.y, d.z};
+    for (int i = 0; i < 2; ++i) {
+      const int c = ch[i];
+      if (c <= N) {
+        add(s, 4, codes(c), CODES + 32 * i, 32);
+        add(s, 2, tcb(c), TC(1 + i), TCBB);
+      } else {
+        const bool kept = s >= 1 && post[size_t(s - 1)].x == c;
+        const bool hand2 = s >= 2 && post[size_t(s - 2)].x == c;
+        if (!kept && !hand2) add(s, 0, slot(c), OP(0), SLOTB);
+      }
+    }
+    if (d.x != root) add(s, 2, tcb(d.x), TC(0), TCBB);
+    const bool next_uses = s + 1 < n && (post[size_t(s + 1)].y == d.x || post[size_t(s + 1)].z == d.x);
+    if (!next_uses && s + 2 < n && (post[size_t(s + 2)].y == d.x || post[size_t(s + 2)].z == d.x))
+      h.flags |= kW4xPostHandE2;
+    add(s, 5, (long long)s * 32, 0, 32);
+  }
+  // ---- pre-order steps
+  auto other = [&](const int4& d) {
+    const int o = d.y == d.w ? d.z : d.y;
+    return o > N ? o : -1;
+  };
+  for (int s = 0; s < n; ++s) {
+    const int k = n + s;
+    const int4 d = pre[size_t(s)];
+    Walk4xHdr& h = hdr[size_t(k)];
+    h.d = d;
+    const bool h1 = d.x == root || (s >= 1 && pre[size_t(s - 1)].w == d.x);
+    const bool h2 = s >= 2 && other(pre[size_t(s - 2)]) == d.x;
+    if (!h1 && !h2) {
+      add(k, 1, slot(d.x), OP(2), SLOTB);
+      h.flags |= kW4xPreQGlobal;
+    }
+    const int ch[2] = {d.y, d.z};
+    for (int i = 0; i < 2; ++i) {
+      const int c = ch[i];
+      if (c <= N) {
+        add(k, 4, codes(c), CODES + 32 * i, 32);
+        add(k, 3, tcb(c), OP(i), TCBB);  // Q P table of the tip
+      } else {
+        add(k, 0, slot(c), OP(i), SLOTB);
+        if (c != d.w && s + 2 < n && pre[size_t(s + 2)].x == c) h.flags |= i == 0 ? kW4xPreHandY2 : kW4xPreHandZ2;
+      }
+    }
+    add(k, 2, tcb(d.y), TC(0), TCBB);
+    add(k, 2, tcb(d.z), TC(1), TCBB);
+    add(k, 5, (long long)k * 32, 0, 32);
+  }
+}
+
+}  // namespace pgk

@@ -8,7 +8,9 @@ patterns (engine.hpp:217, :268), so the chunk sums are the full-size result
 
 Each fixture stores a digest of the generated inputs (so a test can prove it
 regenerated the same instance), logL, the branch-length gradient g, and for the
-clock config the rate gradient dt * g (clock.hpp:146-152, cli.hpp:437-438).
+clock config the rate gradient dt * g (clock.hpp:146-152, cli.hpp:437-438),
+plus each component's condition sum_s w_s |term_s| (the
+scale for components whose per-pattern terms cancel).
 
     python tests/golden/make_fullsize.py [C3 C4 C5]   # minutes per config on 8 cores
 """
@@ -40,6 +42,7 @@ def evaluate_chunked(inst, threads, log=print):
     step = chunk_patterns(inst)
     ll = 0.0
     g = np.zeros(inst.branches)
+    cond = np.zeros(inst.branches)
     t0 = time.time()
     for a in range(0, P, step):
         b = min(P, a + step)
@@ -47,10 +50,11 @@ def evaluate_chunked(inst, threads, log=print):
         lla, ga, _ = ref.branch_gradient(False)
         ll += lla
         g += ga
+        cond += ref.gradient_condition()
         del ref
         if log and (a // step) % 20 == 0:
             log(f"  {inst.name}: {b}/{P} patterns, {time.time() - t0:.0f} s")
-    return ll, g, time.time() - t0, step
+    return ll, g, cond, time.time() - t0, step
 
 
 def main(names):
@@ -61,10 +65,12 @@ def main(names):
         t_gen = time.time() - t0
         dig = synth.instance_digest(inst)
         print(f"{name}: {inst.tip_count} tips, {inst.patterns} patterns, m={inst.states}, generated in {t_gen:.1f} s")
-        ll, g, t_eval, step = evaluate_chunked(inst, threads)
+        ll, g, cond, t_eval, step = evaluate_chunked(inst, threads)
         out = dict(name=name, seed=SEED, digest=dig, patterns=inst.patterns, tips=inst.tip_count,
                    states=inst.states, categories=len(inst.cat_rates), logL=ll, gradient=g,
                    rate_gradient=(inst.durations * g) if inst.clock else np.zeros(0),
+                   gradient_condition=cond,
+                   rate_gradient_condition=(inst.durations * cond) if inst.clock else np.zeros(0),
                    chunk_patterns=step, oracle_seconds=t_eval, oracle_threads=threads)
         np.savez_compressed(os.path.join(HERE, f"full_{name}.npz"), **out)
         print(f"{name}: logL {ll:.10f}, max|g| {np.abs(g).max():.6e}, oracle {t_eval:.0f} s on {threads} threads")

@@ -42,11 +42,15 @@ def test_full_size_workload_matches_oracle(name, kernel, lanes):
     info = eng.info()
     assert info["kernel"] == kernel and info["lanes_per_pattern"] == lanes, info
     want = fx["rate_gradient"] if inst.clock else fx["gradient"]
+    cond = fx["rate_gradient_condition"] if inst.clock else fx["gradient_condition"]
     assert_logl(rep.log_likelihood, float(fx["logL"]))
-    assert_vec(rep.branch_gradient, want, what=f"{name} full-size gradient")
+    # 1e-9 relative per component; a component whose 10^5..10^6 per-pattern
+    # terms cancel is judged against its condition sum_s w_s |term_s|
+    assert_vec(rep.branch_gradient, want, what=f"{name} full-size gradient", cond=cond)
     if inst.clock:
         # the plain branch-length gradient of the same evaluation route
-        assert_vec(eng.branch_gradient().branch_gradient, fx["gradient"], what=f"{name} branch-length gradient")
+        assert_vec(eng.branch_gradient().branch_gradient, fx["gradient"], what=f"{name} branch-length gradient",
+                   cond=fx["gradient_condition"])
 
 
 @pytest.mark.gpu
