@@ -62,11 +62,6 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 // kW4xPreHandY2 / kW4xPreHandZ2 (hand child y / z's q to step s+2).
 // Copy kinds: 0 edge-message scratch (CTA base), 1 pre-partial scratch (CTA
 // base), 2 TC, 3 QTC, 4 tip codes (tile base), 5 step headers.
-struct Walk4xParams {
-  Walk4Params p4;
-  const Walk4xHdr* hdr;    // [2][n] post steps, then pre steps
-  const Walk4xCopy* cpy;   // [2][n][kW4xMaxCopies]
-};
 
 template <int LW, int NC, bool HESS>
 struct Walk4xGeom {

@@ -9,6 +9,8 @@
 
 #include <vector>
 
+#include "pg_walk.cuh"
+
 namespace pgk {
 
 struct Walk4xHdr {
@@ -26,6 +28,12 @@ struct Walk4xCopy {
 constexpr int kW4xPostHandE2 = 1;
 constexpr int kW4xPreQGlobal = 1, kW4xPreHandY2 = 2, kW4xPreHandZ2 = 4;
 constexpr int kW4xMaxCopies = 8;
+
+struct Walk4xParams {
+  Walk4Params p4;
+  const Walk4xHdr* hdr;    // [2][n] post steps, then pre steps
+  const Walk4xCopy* cpy;   // [2][n][kW4xMaxCopies]
+};
 
 // post / pre: the engine's schedules ({node, child, child, next}); N tips, L
 // categories, NC table columns, Pc tip-code row stride.
