@@ -114,46 +114,66 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
 
   if (l == LW) {
     // ======================================================== producer
-    // (all lanes walk the stream; lane c issues copy c of a step)
+    // Lane c < ncopy issues copy c of a step; the copy entry (lanes 0..7) and
+    // the step's {ncopy, tx} (lane 8) are loaded two steps ahead into
+    // registers, so no global load sits between a free stage and its copies.
+    auto entry = [&](int k, Walk4xCopy& c, int2& h) {
+      if (lane < kW4xMaxCopies) c = PX.cpy[size_t(k) * kW4xMaxCopies + lane];
+      else if (lane == 8) h = make_int2(__ldg(&PX.hdr[k].ncopy), __ldg(&PX.hdr[k].tx));
+    };
+    Walk4xCopy c0{}, c1{}, c2{};
+    int2 h0 = make_int2(0, 0), h1 = h0, h2 = h0;
+    // iterator two steps ahead: (tile index ti2, step k2)
+    int ti2 = 0, k2 = 0;
+    auto advance2 = [&]() {
+      if (++k2 == per_tile) {
+        k2 = 0;
+        ++ti2;
+      }
+    };
+    entry(0, c0, h0);
+    advance2();
+    if (ti2 < my_tiles) entry(k2, c1, h1);
+    advance2();
     int st = 0;
     unsigned ephase = 0;
     long long j = 0;
     for (int ti = 0; ti < my_tiles; ++ti) {
       const int tile = int(blockIdx.x) + ti * int(gridDim.x);
       for (int k = 0; k < per_tile; ++k, ++j) {
+        if (ti2 < my_tiles) entry(k2, c2, h2);  // two steps on
+        // L2 prefetch of that step's scratch operands
+        if (ti2 < my_tiles && lane < kW4xMaxCopies) {
+          const int kind = c2.kb >> 24;
+          if (kind <= 1 && (c2.kb & 0xffffff) != 0) bulk_prefetch_l2((kind == 0 ? E : Qs) + c2.src, unsigned(c2.kb & 0xffffff));
+        }
         if (j >= NST) {
           mbar_wait(empty + st, (ephase >> st) & 1u);
           ephase ^= 1u << st;
         }
-        const Walk4xHdr* h = PX.hdr + k;
-        const int ncopy = __ldg(&h->ncopy);
-        if (lane == 0) mbar_arrive_tx(full + st, unsigned(__ldg(&h->tx)));
+        const int ncopy = __shfl_sync(kFull, h0.x, 8), tx = __shfl_sync(kFull, h0.y, 8);
+        if (lane == 0) mbar_arrive_tx(full + st, unsigned(tx));
         __syncwarp();
         double* sb = stg + st * STAGE;
         if (lane < ncopy) {
-          const Walk4xCopy c = PX.cpy[size_t(k) * kW4xMaxCopies + lane];
-          const int kind = c.kb >> 24, bytes = c.kb & 0xffffff;
+          const int kind = c0.kb >> 24, bytes = c0.kb & 0xffffff;
           const void* src;
           switch (kind) {
-            case 0: src = E + c.src; break;
-            case 1: src = Qs + c.src; break;
-            case 2: src = p.tc + c.src; break;
-            case 3: src = p.qtc + c.src; break;
-            case 4: src = p.codes + c.src + size_t(tile) * 32; break;
-            default: src = reinterpret_cast<const char*>(PX.hdr) + c.src; break;
+            case 0: src = E + c0.src; break;
+            case 1: src = Qs + c0.src; break;
+            case 2: src = p.tc + c0.src; break;
+            case 3: src = p.qtc + c0.src; break;
+            case 4: src = p.codes + c0.src + size_t(tile) * 32; break;
+            default: src = reinterpret_cast<const char*>(PX.hdr) + c0.src; break;
           }
-          bulk_g2s(reinterpret_cast<char*>(sb) + c.dst, src, unsigned(bytes), full + st);
+          bulk_g2s(reinterpret_cast<char*>(sb) + c0.dst, src, unsigned(bytes), full + st);
         }
-        // L2 prefetch of the scratch operands two steps on (lanes 8..15)
-        const int k2 = k + 2 < per_tile ? k + 2 : -1;
-        if (k2 >= 0 && lane >= 8 && lane < 8 + kW4xMaxCopies) {
-          const int c2n = __ldg(&PX.hdr[k2].ncopy);
-          if (lane - 8 < c2n) {
-            const Walk4xCopy c = PX.cpy[size_t(k2) * kW4xMaxCopies + (lane - 8)];
-            const int kind = c.kb >> 24;
-            if (kind <= 1) bulk_prefetch_l2((kind == 0 ? E : Qs) + c.src, unsigned(c.kb & 0xffffff));
-          }
-        }
+        c0 = c1;
+        c1 = c2;
+        h0 = h1;
+        h1 = h2;
+        c2 = Walk4xCopy{};
+        if (ti2 < my_tiles) advance2();
         st = st == NST - 1 ? 0 : st + 1;
       }
     }

@@ -42,7 +42,8 @@ def test_full_size_workload_matches_oracle(name, kernel, lanes):
     info = eng.info()
     assert info["kernel"] == kernel and info["lanes_per_pattern"] == lanes, info
     want = fx["rate_gradient"] if inst.clock else fx["gradient"]
-    cond = fx["rate_gradient_condition"] if inst.clock else fx["gradient_condition"]
+    ckey = "rate_gradient_condition" if inst.clock else "gradient_condition"
+    cond = fx[ckey] if ckey in fx.files else None
     assert_logl(rep.log_likelihood, float(fx["logL"]))
     # 1e-9 relative per component; a component whose 10^5..10^6 per-pattern
     # terms cancel is judged against its condition sum_s w_s |term_s|
@@ -50,7 +51,7 @@ def test_full_size_workload_matches_oracle(name, kernel, lanes):
     if inst.clock:
         # the plain branch-length gradient of the same evaluation route
         assert_vec(eng.branch_gradient().branch_gradient, fx["gradient"], what=f"{name} branch-length gradient",
-                   cond=fx["gradient_condition"])
+                   cond=fx["gradient_condition"] if "gradient_condition" in fx.files else None)
 
 
 @pytest.mark.gpu
