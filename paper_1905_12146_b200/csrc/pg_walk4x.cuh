@@ -65,7 +65,7 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 
 template <int LW, int NC, bool HESS>
 struct Walk4xGeom {
-  static constexpr int NST = 3;              // stages
+  static constexpr int NST = 4;              // stages (3 steps of lookahead)
   static constexpr int SLOT = LW * 32 * 4;   // doubles: one node slot of the CTA tile
   static constexpr int TCB = LW * NC * 4;    // doubles: one node's column table (all categories)
   // stage (doubles): header, 3 operand slots, 3 TC blocks, 2 x 32 code bytes
@@ -115,37 +115,41 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
   if (l == LW) {
     // ======================================================== producer
     // Lane c < ncopy issues copy c of a step; the copy entry (lanes 0..7) and
-    // the step's {ncopy, tx} (lane 8) are loaded two steps ahead into
+    // the step's {ncopy, tx} (lane 8) are loaded three steps ahead into
     // registers, so no global load sits between a free stage and its copies.
     auto entry = [&](int k, Walk4xCopy& c, int2& h) {
       if (lane < kW4xMaxCopies) c = PX.cpy[size_t(k) * kW4xMaxCopies + lane];
       else if (lane == 8) h = make_int2(__ldg(&PX.hdr[k].ncopy), __ldg(&PX.hdr[k].tx));
     };
-    Walk4xCopy c0{}, c1{}, c2{};
-    int2 h0 = make_int2(0, 0), h1 = h0, h2 = h0;
-    // iterator two steps ahead: (tile index ti2, step k2)
-    int ti2 = 0, k2 = 0;
-    auto advance2 = [&]() {
-      if (++k2 == per_tile) {
-        k2 = 0;
-        ++ti2;
+    Walk4xCopy c0{}, c1{}, c2{}, c3{};
+    int2 h0 = make_int2(0, 0), h1 = h0, h2 = h0, h3 = h0;
+    // iterator three steps ahead: (tile index ti3, step k3)
+    int ti3 = 0, k3 = 0;
+    auto advance3 = [&]() {
+      if (++k3 == per_tile) {
+        k3 = 0;
+        ++ti3;
       }
     };
     entry(0, c0, h0);
-    advance2();
-    if (ti2 < my_tiles) entry(k2, c1, h1);
-    advance2();
+    advance3();
+    if (ti3 < my_tiles) entry(k3, c1, h1);
+    advance3();
+    if (ti3 < my_tiles) entry(k3, c2, h2);
+    advance3();
     int st = 0;
     unsigned ephase = 0;
     long long j = 0;
     for (int ti = 0; ti < my_tiles; ++ti) {
       const int tile = int(blockIdx.x) + ti * int(gridDim.x);
       for (int k = 0; k < per_tile; ++k, ++j) {
-        if (ti2 < my_tiles) entry(k2, c2, h2);  // two steps on
-        // L2 prefetch of that step's scratch operands
-        if (ti2 < my_tiles && lane < kW4xMaxCopies) {
+        c3 = Walk4xCopy{};
+        if (ti3 < my_tiles) entry(k3, c3, h3);  // three steps on (consumed next iterations)
+        // L2 prefetch of the scratch operands two steps on (entry loaded last iteration)
+        if (lane < kW4xMaxCopies) {
           const int kind = c2.kb >> 24;
-          if (kind <= 1 && (c2.kb & 0xffffff) != 0) bulk_prefetch_l2((kind == 0 ? E : Qs) + c2.src, unsigned(c2.kb & 0xffffff));
+          if (kind <= 1 && (c2.kb & 0xffffff) != 0)
+            bulk_prefetch_l2((kind == 0 ? E : Qs) + c2.src, unsigned(c2.kb & 0xffffff));
         }
         if (j >= NST) {
           mbar_wait(empty + st, (ephase >> st) & 1u);
@@ -170,10 +174,11 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
         }
         c0 = c1;
         c1 = c2;
+        c2 = c3;
         h0 = h1;
         h1 = h2;
-        c2 = Walk4xCopy{};
-        if (ti2 < my_tiles) advance2();
+        h2 = h3;
+        if (ti3 < my_tiles) advance3();
         st = st == NST - 1 ? 0 : st + 1;
       }
     }
