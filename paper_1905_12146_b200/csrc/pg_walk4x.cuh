@@ -20,18 +20,18 @@
 // (cp.async.bulk, TMA engine), one per lane: an internal child's edge-message
 // slot or a deferred pre-partial ([node][cat][lane][4] doubles, LW KB), a
 // node's column table TC ([cat][NC][4] doubles), a tip's 32 code bytes, a
-// tip's Q P table, and the header itself.  Three stages give two steps of
-// lookahead; the scratch operands of the step after those are prefetched
-// into L2.
+// tip's Q P table, and the header itself.  Four stages give three steps of
+// lookahead; the scratch operands two steps on are also prefetched into L2.
 //
 // Hand-offs (consumer warps).  A value produced by step i and consumed by
-// step i+1 or i+2 of the same pass never goes through global memory for that
-// use: the producing warp writes its category slice straight into the
-// consumer's stage (post: the edge message of step i+1 stays in registers;
-// pre: the child's pre-partial; the root's pi for the first pre-order step).
-// Anything consumed later was stored at least three steps before its copy is
-// issued; its writer fenced it (fence.proxy.async) before arriving on the
-// stage's `empty` barrier that the producer waited on.
+// step i+1..i+3 of the same pass (the producer may run that far ahead)
+// never goes through global memory for that use: the producing warp writes
+// its category slice straight into the consumer's stage (post: the edge
+// message of step i+1 stays in registers; pre: the child's pre-partial; the
+// root's pi for the first pre-order step).  Anything consumed later was
+// stored at least four steps before its copy is issued; its writer fenced it
+// (fence.proxy.async) before arriving on the stage's `empty` barrier that the
+// producer waited on.
 //
 // Cross-category quantities go through a small shared exchange (double-
 // buffered by step parity) with one consumer barrier per step: the
@@ -57,15 +57,13 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 }
 
 // Step headers and copy lists: pg_walk4x_tables.hpp (built on the host).
-// Header flags: post: kW4xPostHandE2 (hand this node's e to step s+2's
-// stage); pre: kW4xPreQGlobal (q staged from scratch: drop it after use),
-// kW4xPreHandY2 / kW4xPreHandZ2 (hand child y / z's q to step s+2).
+// Header flags: hand-off distances and the pre-order q source (see there).
 // Copy kinds: 0 edge-message scratch (CTA base), 1 pre-partial scratch (CTA
 // base), 2 TC, 3 QTC, 4 tip codes (tile base), 5 step headers.
 
 template <int LW, int NC, bool HESS>
 struct Walk4xGeom {
-  static constexpr int NST = 4;              // stages (3 steps of lookahead)
+  static constexpr int NST = kW4xHand + 1;   // stages: kW4xHand steps of lookahead
   static constexpr int SLOT = LW * 32 * 4;   // doubles: one node slot of the CTA tile
   static constexpr int TCB = LW * NC * 4;    // doubles: one node's column table (all categories)
   // stage (doubles): header, 3 operand slots, 3 TC blocks, 2 x 32 code bytes
@@ -236,7 +234,9 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
     int S = 0;  // post: accumulated exponent of the tile's patterns
     last = -1;
     for (int k = 0; k < per_tile; ++k, ++j) {
-      const int st1 = st == NST - 1 ? 0 : st + 1, st2 = st1 == NST - 1 ? 0 : st1 + 1;
+      const int st1 = st == NST - 1 ? 0 : st + 1;
+      // stage of the step `dist` on (hand-offs)
+      auto stage_on = [&](int dist) { return st + dist >= NST ? st + dist - NST : st + dist; };
       mbar_wait(full + st, (fphase >> st) & 1u);
       fphase ^= 1u << st;
       const Walk4xHdr& H = *reinterpret_cast<const Walk4xHdr*>(stg + st * STAGE + Gx::HDR);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
           __stcs(dst, make_double2(e0, e1));
           __stcs(dst + 32, make_double2(e2, e3));
           // consumed two steps on: straight into that step's stage
-          if (flags & kW4xPostHandE2) wr4_smem(op(st2, 0), keep, 1.0);
+          if ((flags & 3) >= 2) wr4_smem(op(stage_on(flags & 3), 0), keep, 1.0);
           last = d.x;
         }
       } else {
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
         // normalise (shared peak over the categories) and hand on: the child
         // visited next through the next stage's q slot, a child visited two
         // steps on through that stage's, any other to scratch
-        auto emit = [&](int x, const double (&qx)[4], int field, bool hand2) {
+        auto emit = [&](int x, const double (&qx)[4], int field, int dist) {
           int hx = xint[(field * 32 + lane) * LW];
 #pragma unroll
           for (int c = 1; c < LW; ++c) hx = max(hx, xint[(field * 32 + lane) * LW + c]);
@@ -485,16 +485,16 @@ __global__ void __launch_bounds__(32 * (LW + 1), (LW >= 4 ? 3 : 8))
           const double scl = (ex != 0 && ex <= 1022) ? pow2_neg(ex) : 1.0;
           if (x == d.w) {
             wr4_smem(op(st1, 2), qx, scl);
-          } else if (hand2) {
-            wr4_smem(op(st2, 2), qx, scl);
+          } else if (dist >= 2) {
+            wr4_smem(op(stage_on(dist), 2), qx, scl);
           } else {
             double2* dst = reinterpret_cast<double2*>(Qs + size_t(x - N - 1) * SLOT + l * 128) + lane;
             __stcg(dst, make_double2(qx[0] * scl, qx[1] * scl));
             __stcg(dst + 32, make_double2(qx[2] * scl, qx[3] * scl));
           }
         };
-        if (a_int) emit(d.y, qa, 0, flags & kW4xPreHandY2);
-        if (b_int) emit(d.z, qb, 1, flags & kW4xPreHandZ2);
+        if (a_int) emit(d.y, qa, 0, (flags >> 1) & 3);
+        if (b_int) emit(d.z, qb, 1, (flags >> 3) & 3);
       }
       // this step's stage is consumed: its scratch stores are fenced for the
       // async proxy (bulk copies issued after the producer sees `empty`)

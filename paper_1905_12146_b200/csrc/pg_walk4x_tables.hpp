@@ -25,8 +25,15 @@ struct Walk4xCopy {
   int dst;
   int kb;
 };
-constexpr int kW4xPostHandE2 = 1;
-constexpr int kW4xPreQGlobal = 1, kW4xPreHandY2 = 2, kW4xPreHandZ2 = 4;
+// Header flags.  Hand-off distances (0: none) are 2 bit fields: a value
+// produced at step i and consumed at step i + dist (dist <= kW4xHand, one
+// less than the stage count) is written by the consumer warps straight into
+// that step's stage instead of going through scratch + a bulk copy.
+//   post: bits 0-1 distance of this node's edge message (1 = kept in registers)
+//   pre:  bit 0 q staged from scratch (drop it after use);
+//         bits 1-2 / 3-4 distance of child y's / z's pre-partial
+constexpr int kW4xPreQGlobal = 1;
+constexpr int kW4xHand = 3;
 constexpr int kW4xMaxCopies = 8;
 
 struct Walk4xParams {
@@ -71,15 +78,17 @@ inline void build_walk4x_tables(const std::vector<int4>& post, const std::vector
         add(s, 4, codes(c), CODES + 32 * i, 32);
         add(s, 2, tcb(c), TC(1 + i), TCBB);
       } else {
-        const bool kept = s >= 1 && post[size_t(s - 1)].x == c;
-        const bool hand2 = s >= 2 && post[size_t(s - 2)].x == c;
-        if (!kept && !hand2) add(s, 0, slot(c), OP(0), SLOTB);
+        bool handed = false;  // produced within the last kW4xHand steps: in registers / handed on
+        for (int dist = 1; dist <= kW4xHand && s - dist >= 0; ++dist) handed = handed || post[size_t(s - dist)].x == c;
+        if (!handed) add(s, 0, slot(c), OP(0), SLOTB);
       }
     }
     if (d.x != root) add(s, 2, tcb(d.x), TC(0), TCBB);
-    const bool next_uses = s + 1 < n && (post[size_t(s + 1)].y == d.x || post[size_t(s + 1)].z == d.x);
-    if (!next_uses && s + 2 < n && (post[size_t(s + 2)].y == d.x || post[size_t(s + 2)].z == d.x))
-      h.flags |= kW4xPostHandE2;
+    for (int dist = 1; dist <= kW4xHand && s + dist < n; ++dist)
+      if (post[size_t(s + dist)].y == d.x || post[size_t(s + dist)].z == d.x) {
+        h.flags |= dist;
+        break;
+      }
     add(s, 5, (long long)s * 32, 0, 32);
   }
   // ---- pre-order steps
@@ -92,9 +101,9 @@ inline void build_walk4x_tables(const std::vector<int4>& post, const std::vector
     const int4 d = pre[size_t(s)];
     Walk4xHdr& h = hdr[size_t(k)];
     h.d = d;
-    const bool h1 = d.x == root || (s >= 1 && pre[size_t(s - 1)].w == d.x);
-    const bool h2 = s >= 2 && other(pre[size_t(s - 2)]) == d.x;
-    if (!h1 && !h2) {
+    bool handed = d.x == root || (s >= 1 && pre[size_t(s - 1)].w == d.x);
+    for (int dist = 2; dist <= kW4xHand && s - dist >= 0; ++dist) handed = handed || other(pre[size_t(s - dist)]) == d.x;
+    if (!handed) {
       add(k, 1, slot(d.x), OP(2), SLOTB);
       h.flags |= kW4xPreQGlobal;
     }
@@ -106,7 +115,12 @@ inline void build_walk4x_tables(const std::vector<int4>& post, const std::vector
         add(k, 3, tcb(c), OP(i), TCBB);  // Q P table of the tip
       } else {
         add(k, 0, slot(c), OP(i), SLOTB);
-        if (c != d.w && s + 2 < n && pre[size_t(s + 2)].x == c) h.flags |= i == 0 ? kW4xPreHandY2 : kW4xPreHandZ2;
+        if (c != d.w)
+          for (int dist = 2; dist <= kW4xHand && s + dist < n; ++dist)
+            if (pre[size_t(s + dist)].x == c) {
+              h.flags |= dist << (1 + 2 * i);
+              break;
+            }
       }
     }
     add(k, 2, tcb(d.y), TC(0), TCBB);
