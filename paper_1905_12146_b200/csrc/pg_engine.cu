@@ -574,10 +574,12 @@ struct pg_engine {
       G = L / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);
       const size_t tcb = size_t(L) * NC * 4;
-      // category-parallel variant: warp l of a CTA holds category l of a
-      // 32-pattern tile (PG_WALK4X=0 keeps the per-warp walk4 for A/B runs)
+      // category-parallel, warp-specialised variant (pg_walk4x.cuh): opt-in
+      // with PG_WALK4X=1 -- measured slower than walk4 on C2 / C3 (C3 250 vs
+      // 152 ms: the per-step control work is repeated by every category warp,
+      // 1.8x the instructions)
       const char* wx = std::getenv("PG_WALK4X");
-      use_walk4x = (wx == nullptr || std::atoi(wx) != 0) &&
+      use_walk4x = (wx != nullptr && std::atoi(wx) != 0) &&
                    pg_walk4x_kernel(branch_q.empty(), false, NC, L, &walk_smem) != nullptr;
       if (use_walk4x) {
         G = 1;

@@ -1,8 +1,8 @@
 """Direct oracle parity of every 4-state walk variant (the C2/C3 bench
-kernels): the category-parallel walk4x_kernel<HOMOG, HESS, NC, L> (default
-for 4 categories: warp l of a CTA holds category l of a 32-pattern tile) and
-the per-warp walk4_kernel<HOMOG, HESS, NC, LCV> with one lane per pattern
-(LCV=4) or two (LCV=2) forced through PG_WALK4X=0 / PG_WALK4_LCV;
+kernels): the per-warp walk4_kernel<HOMOG, HESS, NC, LCV> with one lane per
+pattern (LCV=4) or two (LCV=2) forced through PG_WALK4_LCV, and the opt-in
+category-parallel walk4x_kernel<HOMOG, HESS, NC, L> (PG_WALK4X=1: warp l of
+a CTA holds category l of a 32-pattern tile, a producer warp stages);
 homogeneous and per-branch generators, with and without the Hessian, gaps
 only (NC=5) and IUPAC ambiguity classes (NC=16).  walk4x evaluates walk4's
 arithmetic chains in the same order, so the two agree bit for bit."""
@@ -24,7 +24,7 @@ from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCate
 def lcv(request, monkeypatch):
     """The kernel variant under test; returns (kernel name, lanes per pattern)."""
     if request.param == "cat":
-        monkeypatch.delenv("PG_WALK4X", raising=False)
+        monkeypatch.setenv("PG_WALK4X", "1")
         return "walk4x_kernel", 1
     monkeypatch.setenv("PG_WALK4X", "0")
     monkeypatch.setenv("PG_WALK4_LCV", str(request.param))
@@ -176,7 +176,7 @@ def test_walk4x_matches_walk4(monkeypatch, name, sites, hess):
     e4, _ = _instance_pair(inst)
     r4 = e4.branch_gradient(hess)
     assert e4.info()["kernel"] == "walk4_kernel"
-    monkeypatch.delenv("PG_WALK4X")
+    monkeypatch.setenv("PG_WALK4X", "1")
     ex, _ = _instance_pair(inst)
     rx = ex.branch_gradient(hess)
     assert ex.info()["kernel"] == "walk4x_kernel"
