@@ -1117,6 +1117,7 @@ class Engine {
     if (hess) hessd_.assign(size_t(tree_.branch_count()), 0.0);
     Mat buffer(m, P_), qp(m, P_);
     Vec u1(static_cast<size_t>(P_)), u2(static_cast<size_t>(P_)), r1(static_cast<size_t>(P_));
+    Vec u1abs(static_cast<size_t>(P_));  // the same sums over absolute values (condition)
     for (int node : tree_.pre_order) {
       ++visits_;
       if (node == tree_.root()) {
@@ -1147,6 +1148,7 @@ class Engine {
       rescale(pre_[size_t(node)], sc);
 
       std::fill(u1.begin(), u1.end(), 0.0);
+      std::fill(u1abs.begin(), u1abs.end(), 0.0);
       if (hess) std::fill(u2.begin(), u2.end(), 0.0);
       const Mat& Q = model_.generator(node);
       const Mat Q2 = hess ? q2_for(node) : Mat();
@@ -1155,17 +1157,20 @@ class Engine {
         const Mat& pm = post_matrix(node, l);
         const Mat& q = pre_[size_t(node)][size_t(l)];
         for (int s = 0; s < P_; ++s) {
-          double acc = 0.0, acc2 = 0.0;
+          double acc = 0.0, acc2 = 0.0, acca = 0.0;
           for (int i = 0; i < m; ++i) {
-            double qpi = 0.0, q2pi = 0.0;
+            double qpi = 0.0, q2pi = 0.0, qpa = 0.0;
             for (int j = 0; j < m; ++j) {
               qpi += Q(i, j) * pm(j, s);
+              qpa += std::fabs(Q(i, j) * pm(j, s));
               if (hess) q2pi += Q2(i, j) * pm(j, s);
             }
             acc += qpi * q(i, s);
+            acca += qpa * std::fabs(q(i, s));
             acc2 += q2pi * q(i, s);
           }
           u1[size_t(s)] += (cl * wl) * acc;
+          u1abs[size_t(s)] += (cl * wl) * acca;
           if (hess) u2[size_t(s)] += (cl * cl * wl) * acc2;
         }
       }
@@ -1174,7 +1179,10 @@ class Engine {
         const double e = std::exp(scaler_post_[size_t(node)][size_t(s)] + scaler_pre_[size_t(node)][size_t(s)] - site_ll_[size_t(s)]);
         r1[size_t(s)] = u1[size_t(s)] * e;
         g += weights_[size_t(s)] * r1[size_t(s)];
-        ga += weights_[size_t(s)] * std::fabs(r1[size_t(s)]);  // condition of the sum (test use)
+        // condition of the component (test use): every product of the
+        // per-pattern term taken in absolute value, so cancellation inside
+        // Q e (rows of Q sum to zero) and across patterns both count
+        ga += weights_[size_t(s)] * u1abs[size_t(s)] * e;
         if (hess) {
           const double r2 = u2[size_t(s)] * e;
           hd += weights_[size_t(s)] * (r2 - r1[size_t(s)] * r1[size_t(s)]);

@@ -512,9 +512,11 @@ class Engine:
         return ll.value, g, (h if with_hessian else None)
 
     def gradient_condition(self):
-        """sum_s w_s |term_{s,i}| per branch of the last gradient pass: the
-        scale against which a cancelling component's rounding is judged
-        (SURVEY.md §8d condition-aware parity)."""
+        """Per branch of the last gradient pass, the gradient sum with every
+        product of each per-pattern term taken in absolute value (sum_s w_s
+        sum_l c_l w_l sum_i |q_i| sum_j |Q_ij e_j| / L_s): the scale against
+        which a component whose terms cancel -- inside Q e or across
+        patterns -- is judged (SURVEY.md §8d condition-aware parity)."""
         out = np.zeros(self.B)
         _check(lib().orc_engine_gradient_abs(self.h, out))
         return out

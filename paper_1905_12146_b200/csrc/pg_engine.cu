@@ -22,6 +22,7 @@
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
 #include "pg_walk4x_tables.hpp"
+#include "pg_walkl.cuh"
 
 void* pg_walk4_kernel_lc4(bool homog, bool hess, int nc);
 void* pg_walk4_kernel_lc2(bool homog, bool hess, int nc);
@@ -33,6 +34,7 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
 }
 int pg_walk4_nc(int nc);
 void* pg_walk4x_kernel(bool homog, bool hess, int nc, int L, size_t* smem);
+void* pg_walkl_kernel(int L, bool homog, bool hess);
 void* pg_walkm_kernel(int mp, bool hess);
 size_t pg_walkm_smem(int mp);
 int pg_walkm_wpc(int mp);
@@ -134,6 +136,11 @@ struct pg_engine {
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
   bool use_walk4x = false;  // category-parallel 4-state walk (pg_walk4x.cuh): one CTA of L warps per tile
+  bool use_walkl = false;   // level-scheduled 4-state traversal (pg_walkl.cuh): small P
+  int walkl_max_patterns_per_sm = 16;  // P below this x SMs: level-scheduled (overridable: PG_WALKL)
+  int walkl_npost = 0, walkl_npre = 0, walkl_grid = 0;
+  DevBuf<int> d_lvl_nodes, d_lvl_off, d_Sx;
+  DevBuf<unsigned> d_bar;
   bool use_walkm = false;  // DMMA large-state kernel (pg_walkm.cuh)
   int codes_mp = 0;        // MP the device tip codes' class columns are encoded for
   int walkm_wpc = 4;       // warps per CTA in walkm
@@ -281,6 +288,44 @@ struct pg_engine {
       }
       pre_steps[i].w = next;
     }
+  }
+
+  // Level lists of the level-scheduled traversal (pg_walkl.cuh): internal
+  // nodes by height (post-order levels: a node needs only its children) and
+  // by depth (pre-order levels: a node needs only its parent).
+  void build_levels() {
+    const int n = 2 * N - 1;
+    std::vector<int> height(size_t(n + 1), 0), depth(size_t(n + 1), 0);
+    for (const int4& st : post_steps) height[size_t(st.x)] = 1 + std::max(height[size_t(st.y)], height[size_t(st.z)]);
+    for (const int4& st : pre_steps) {
+      depth[size_t(st.y)] = depth[size_t(st.x)] + 1;
+      depth[size_t(st.z)] = depth[size_t(st.x)] + 1;
+    }
+    int H = 0, D = 0;
+    for (const int4& st : post_steps) {
+      H = std::max(H, height[size_t(st.x)]);
+      D = std::max(D, depth[size_t(st.x)]);
+    }
+    std::vector<std::vector<int>> by_h(size_t(H + 1)), by_d(size_t(D + 1));
+    for (const int4& st : post_steps) {
+      by_h[size_t(height[size_t(st.x)])].push_back(st.x);
+      by_d[size_t(depth[size_t(st.x)])].push_back(st.x);
+    }
+    std::vector<int> nodes, off;
+    off.push_back(0);
+    for (int h = 1; h <= H; ++h) {
+      nodes.insert(nodes.end(), by_h[size_t(h)].begin(), by_h[size_t(h)].end());
+      off.push_back(int(nodes.size()));
+    }
+    walkl_npost = H;
+    off.push_back(int(nodes.size()));
+    for (int d = 0; d <= D; ++d) {
+      nodes.insert(nodes.end(), by_d[size_t(d)].begin(), by_d[size_t(d)].end());
+      off.push_back(int(nodes.size()));
+    }
+    walkl_npre = D + 1;
+    d_lvl_nodes.upload(nodes.data(), nodes.size(), stream);
+    d_lvl_off.upload(off.data(), off.size(), stream);
   }
 
   void set_patterns(int mm, int np, const int8_t* codes, int na, const double* ambig, const int64_t* w) {
@@ -560,6 +605,17 @@ struct pg_engine {
                           : (L == 1 || ((L == 2 || L == 3 || L == 8) && int64_t(P) / tp >= int64_t(num_sms))));
     }
     walk_smem = 0;
+    // level-scheduled traversal when the pattern tiles cannot fill the GPU:
+    // walk4's unit is a 16- or 32-pattern tile walking ~2N dependent steps,
+    // so with fewer than ~2 tiles per SM (C2 on 8 GPUs: ~2,500 patterns)
+    // node-level parallelism pays (PG_WALKL=0/1 forces the choice)
+    {
+      const char* wl = std::getenv("PG_WALKL");
+      const bool want = wl ? std::atoi(wl) != 0 : int64_t(P) <= int64_t(walkl_max_patterns_per_sm) * num_sms;
+      use_walkl = MP == 4 && !opt.capture_partials && P > 0 && (L == 1 || L == 2 || L == 4 || L == 8) && want &&
+                  pg_walkl_kernel(L, branch_q.empty(), false) != nullptr;
+    }
+    if (use_walkl) use_walk4 = false;
     if (use_walk4) {
       NC = nc4;  // TC blocks padded with zero columns to the instantiated width
       // one lane per pattern unless that leaves fewer than ~2 tiles per
@@ -589,8 +645,13 @@ struct pg_engine {
                     sizeof(double2);
       }
     }
+    if (use_walkl) {
+      G = L;
+      ntiles = (P + 32 / L - 1) / (32 / L);  // accumulator rows: one per pattern tile
+      build_levels();
+    }
     if (use_walkm) {
-      use_walk4 = use_walk4x = false;
+      use_walk4 = use_walk4x = use_walkl = false;
       LC = 1;
       G = 4;  // a quad of lanes per pattern (DMMA fragment layout)
       walkm_wpc = pg_walkm_wpc(MP);
@@ -601,6 +662,21 @@ struct pg_engine {
     // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents;
     // walk4x: one CTA tile's slot (L categories x 32 patterns x 4 states)
     const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : use_walk4x ? size_t(L) * 32 * 4 : size_t(32) * LC * MP;
+    if (use_walkl) {
+      // every internal node's e and q for all patterns; one accumulator row per tile
+      TW = ntiles;
+      walkl_grid = maxw / pgk::kWarpsPerBlock;  // all co-resident CTAs (cooperative launch)
+      accw = 1 + 2 * B();
+      const size_t all = size_t(std::max(N - 1, 1)) * size_t(P) * size_t(L) * 4;
+      d_escr.ensure(all);
+      d_qscr.ensure(all);
+      d_Sx.ensure(size_t(std::max(N - 1, 1)) * size_t(P));
+      if (d_bar.n < 2) {
+        d_bar.ensure(2);
+        PG_CUDA(cudaMemsetAsync(d_bar.p, 0, 2 * sizeof(unsigned), stream));
+      }
+      d_children.upload(children.data(), children.size(), stream);
+    }
     const size_t per_warp = size_t(std::max(N - 1, 1)) * vec * sizeof(double) * 2;
     // The grid (and with it the fixed-order reduction over warp rows) must
     // not depend on the run-time memory state, or results would not be
@@ -614,7 +690,9 @@ struct pg_engine {
     }
     const size_t budget = size_t(double(total_b) * 0.6);
     int cap = int(std::max<size_t>(1, budget / per_warp));
-    if (use_walkm) {
+    if (use_walkl) {
+      // set above
+    } else if (use_walkm) {
       // CTA tiles: 4 warps per tile
       int ctas = std::max(1, std::min({maxw / walkm_wpc, std::max(ntiles, 1), std::max(cap / walkm_wpc, 1)}));
       TW = ctas * walkm_wpc;
@@ -625,15 +703,17 @@ struct pg_engine {
       TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
     }
     accw = 1 + 2 * B();
-    d_escr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
-    d_qscr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
+    if (!use_walkl) {
+      d_escr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
+      d_qscr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
+    }
     d_acc.ensure(size_t(TW) * size_t(accw));
     d_out.ensure(size_t(accw));
     d_site_ll.ensure(size_t(std::max(P, 1)));
     d_err.ensure(3);
     d_tc.ensure(size_t(B()) * L * NC * MP);
     // Q P column tables: tip Q e in walkm, and in walk4's pre-order pass
-    if (use_walkm || use_walk4) d_qtc.ensure(size_t(B()) * L * NC * MP);
+    if (use_walkm || use_walk4 || use_walkl) d_qtc.ensure(size_t(B()) * L * NC * MP);
     if (use_walkm) {
       const size_t frag = size_t(MP / 4) * ((MP / 4 + 1) / 2) * 32;  // WalkMGeom<MP>::FRAG
       d_fpp.ensure(size_t(B()) * L * frag);
@@ -868,6 +948,14 @@ int pg_engine::walk_max_blocks_per_sm() {
     }
     return std::max(nb, 1);
   }
+  if (use_walkl) {
+    for (int v = 0; v < 2; ++v) {
+      int b = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pg_walkl_kernel(L, branch_q.empty(), v & 1), 256, 0));
+      nb = v == 0 ? b : std::min(nb, b);
+    }
+    return std::max(nb, 1);
+  }
   if (use_walk4x) {
     for (int v = 0; v < 2; ++v) {
       size_t sm = 0;
@@ -905,7 +993,7 @@ void pg_engine::launch_tc() {
   p.eig_w = d_ew.p;
   p.amb = d_amb.p;
   p.tc = d_tc.p;
-  p.qtc = (use_walkm || use_walk4) ? d_qtc.p : nullptr;
+  p.qtc = (use_walkm || use_walk4 || use_walkl) ? d_qtc.p : nullptr;
   p.fpp = use_walkm ? d_fpp.p : nullptr;
   p.fpt = use_walkm ? d_fpt.p : nullptr;
   p.err = d_err.p;
@@ -928,7 +1016,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
   p.codes = d_codes.p;
   p.weights = d_weights.p;
   p.tc = d_tc.p;
-  p.qtc = (use_walkm || use_walk4) ? d_qtc.p : nullptr;
+  p.qtc = (use_walkm || use_walk4 || use_walkl) ? d_qtc.p : nullptr;
   p.qtab = d_qtab.p;
   p.qidx = d_qidx.p;
   p.pi = d_pi.p;
@@ -972,6 +1060,30 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     void* fn = pg_walkm_kernel(MP, do_hess);
     void* args[] = {&pm};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / walkm_wpc)), dim3(32 * walkm_wpc), args, walk_smem, stream));
+    return;
+  }
+  if (use_walkl) {
+    pgk::WalkLParams pl{};
+    pl.p = p;
+    for (int i = 0; i < 4; ++i) {
+      pl.pi[i] = i < m ? pi[size_t(i)] : 0.0;
+      for (int j = 0; j < 4; ++j) pl.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
+    }
+    pl.lvl_nodes = d_lvl_nodes.p;
+    pl.lvl_off = d_lvl_off.p;
+    pl.npost = walkl_npost;
+    pl.npre = walkl_npre;
+    pl.children = d_children.p;
+    pl.E = d_escr.p;
+    pl.Qp = d_qscr.p;
+    pl.Sx = d_Sx.p;
+    pl.bar = d_bar.p;
+    pl.ntp = ntiles;
+    void* fn = pg_walkl_kernel(L, branch_q.empty(), do_hess);
+    // every CTA resident (grid barrier between levels): cooperative launch
+    const int grid = walkl_grid;
+    void* args[] = {&pl};
+    PG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(grid)), dim3(256), args, 0, stream));
     return;
   }
   if (use_walk4) {
@@ -1507,7 +1619,7 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
 
 int pg_engine_variant(const pg_engine* e) {
   e = primary(e);
-  return e->use_walkm ? 2 : e->use_walk4x ? 3 : e->use_walk4 ? 1 : 0;
+  return e->use_walkm ? 2 : e->use_walk4x ? 3 : e->use_walkl ? 4 : e->use_walk4 ? 1 : 0;
 }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {

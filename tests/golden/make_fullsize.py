@@ -9,8 +9,10 @@ patterns (engine.hpp:217, :268), so the chunk sums are the full-size result
 Each fixture stores a digest of the generated inputs (so a test can prove it
 regenerated the same instance), logL, the branch-length gradient g, and for the
 clock config the rate gradient dt * g (clock.hpp:146-152, cli.hpp:437-438),
-plus each component's condition sum_s w_s |term_s| (the
-scale for components whose per-pattern terms cancel).
+plus each component's condition: the same sum with every
+product of the per-pattern term taken in absolute value (oracle
+gradient_condition), the scale for components whose terms cancel — inside
+Q e (generator rows sum to zero) or across patterns.
 
     python tests/golden/make_fullsize.py [C3 C4 C5]   # minutes per config on 8 cores
 """

@@ -9,10 +9,11 @@ from oracle import oracle as O
 # scale (condition-aware variant).
 RTOL = 1e-9
 ATOL_REL_SCALE = 1e-12
-# condition-aware bound: a component whose per-pattern terms
-# cancel is judged against sum_s w_s |term_s| (the oracle's
-# gradient_condition): fp64 summation of n terms in a different order
-# differs by up to ~n eps of that sum, so 1e-11 of it is rounding, not error
+# condition-aware bound: a component whose terms cancel is
+# judged against its condition (the oracle's gradient_condition: the same
+# sums over absolute values, inside Q e and over patterns): evaluating them
+# in a different order differs by up to ~n eps of that scale, so 1e-11 of it
+# is rounding, not error
 COND_RTOL = 1e-11
 
 

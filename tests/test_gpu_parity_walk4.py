@@ -20,9 +20,13 @@ from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCate
                                        SitePatternAlignment, SubstitutionModel, Tree, parse_fasta, parse_newick)
 
 
-@pytest.fixture(params=["cat", 4, 2], ids=["walk4x", "lcv4", "lcv2"])
+@pytest.fixture(params=["cat", "lvl", 4, 2], ids=["walk4x", "walkl", "lcv4", "lcv2"])
 def lcv(request, monkeypatch):
     """The kernel variant under test; returns (kernel name, lanes per pattern)."""
+    if request.param == "lvl":
+        monkeypatch.setenv("PG_WALKL", "1")
+        return "walkl_kernel", 4
+    monkeypatch.setenv("PG_WALKL", "0")
     if request.param == "cat":
         monkeypatch.setenv("PG_WALK4X", "1")
         return "walk4x_kernel", 1
@@ -130,10 +134,14 @@ def _gtr(rng):
 
 @pytest.mark.parametrize("L", [1, 2, 3, 8])
 @pytest.mark.parametrize("homog", [True, False], ids=["homog", "per_branch_q"])
-def test_walk4_other_category_counts(L, homog):
+@pytest.mark.parametrize("level", [False, True], ids=["walk4", "walkl"])
+def test_walk4_other_category_counts(L, homog, level, monkeypatch):
     """The pipelined kernel for 1, 2, 3 rate categories (one lane per pattern)
-    and 8 (two lanes per pattern), with gaps, per-branch generators and the
-    Hessian."""
+    and 8 (two lanes per pattern), and the level-scheduled one for 1, 2, 8
+    (L = 3 has no level-scheduled instance: walk4 runs), with gaps,
+    per-branch generators and the Hessian."""
+    monkeypatch.setenv("PG_WALKL", "1" if level else "0")
+    want_kernel = "walkl_kernel" if level and L != 3 else "walk4_kernel"
     rng = np.random.default_rng(60 + L)
     q, pi = _gtr(rng)
     mo = O.Model(q, pi, True)
@@ -157,7 +165,7 @@ def test_walk4_other_category_counts(L, homog):
     for hess in (False, True):
         ll, g, h = ref.branch_gradient(hess)
         rep = eng.branch_gradient(hess)
-        assert eng.info()["kernel"] == "walk4_kernel"
+        assert eng.info()["kernel"] == want_kernel
         assert_logl(rep.log_likelihood, ll)
         assert_vec(rep.branch_gradient, g)
         if hess:
@@ -184,3 +192,22 @@ def test_walk4x_matches_walk4(monkeypatch, name, sites, hess):
     assert_vec(rx.branch_gradient, r4.branch_gradient, rtol=1e-12)
     if hess:
         assert_vec(rx.hessian_diagonal, r4.hessian_diagonal, rtol=1e-11, what="hessian")
+
+
+@pytest.mark.parametrize("sites", [2500, 600])
+def test_walkl_small_pattern_counts(sites, monkeypatch):
+    """The small-P regime the level-scheduled traversal is for (C2 sliced to
+    one GPU's share at 8 GPUs, and smaller), against the oracle, and
+    bit-reproducible run to run."""
+    monkeypatch.setenv("PG_WALKL", "1")
+    inst = synth.generate("C2", sites=sites)
+    eng, ref = _instance_pair(inst)
+    ll, g, h = ref.branch_gradient(True)
+    rep = eng.branch_gradient(True)
+    assert eng.info()["kernel"] == "walkl_kernel"
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    eng.invalidate_caches()
+    rep2 = eng.branch_gradient(True)
+    assert rep2.log_likelihood == rep.log_likelihood and np.array_equal(rep2.branch_gradient, rep.branch_gradient)
