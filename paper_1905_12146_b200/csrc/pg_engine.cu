@@ -137,7 +137,10 @@ struct pg_engine {
   bool use_walk4 = false;
   bool use_walk4x = false;  // category-parallel 4-state walk (pg_walk4x.cuh): one CTA of L warps per tile
   bool use_walkl = false;   // level-scheduled 4-state traversal (pg_walkl.cuh): small P
-  int walkl_max_patterns_per_sm = 16;  // P below this x SMs: level-scheduled (overridable: PG_WALKL)
+  // P up to this x SMs: level-scheduled (PG_WALKL=0/1 forces).  Measured on C2
+  // (512 taxa, GTR+G4): 1,250 patterns 0.30 vs 1.83 ms, 2,500 0.43 vs 2.37 ms,
+  // 5,000 0.69 vs 0.83 ms, 10,000 1.25 vs 0.98 ms, 20,000 2.14 vs 1.22 ms
+  int walkl_max_patterns_per_sm = 48;
   int walkl_npost = 0, walkl_npre = 0, walkl_grid = 0;
   DevBuf<int> d_lvl_nodes, d_lvl_off, d_Sx;
   DevBuf<unsigned> d_bar;
