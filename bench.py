@@ -155,18 +155,19 @@ def profiled_traffic(config, patterns, world):
 
 
 def roofline_block(inst, patterns, walk_ms, kernel, world, config):
-    """Roofline of the dominant kernel (the walk).  The bound follows the
-    arithmetic intensity F_alg / B_alg against the ridge of the measured
-    peaks (fp64 DMMA / HBM): 4-state models are HBM-bound (1.5 flop/B), the
-    20- and 61-state ones fp64-tensor-bound (7.5 and 22.9 flop/B vs a ridge
-    of ~5.7)."""
+    """Roofline of the dominant kernel (the walk), bound as BASELINE.json's
+    north star frames it: HBM bandwidth for the 4- and 20-state models, the
+    fp64 tensor (DMMA) peak for codons.  The arithmetic intensity F_alg /
+    B_alg and the ridge of the measured peaks are reported beside it (the
+    20-state model sits above the ridge at its design-floor traffic, so its
+    HBM fraction is bounded well below one)."""
     hbm, hbm_src = measured_peaks()
     tf, tf_src = fp64_tensor_peak()
     balg, falg = bytes_alg(inst, patterns), flops_alg(inst, patterns)
     t = walk_ms * 1e-3
     ridge = tf * 1e12 / (hbm * 1e9)
     prof = profiled_traffic(config, inst.patterns, world)
-    if falg / balg > ridge:
+    if inst.states > 32:
         achieved = falg / t / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s", "frac": achieved / tf,
                 "peak_source": tf_src}
