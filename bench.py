@@ -439,8 +439,10 @@ def run_device(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_gen = time.perf_counter()
+    # columns simulated and compressed on this rank's GPU (counter-stream
+    # configs; the reference arm builds the identical instance on the host)
     inst = synth.generate_shared(args.config, rank, world, (lambda: torch.distributed.barrier()) if world > 1 else None,
-                                 tag=str(os.getppid()), seed=SEED, sites=args.sites)
+                                 tag=str(os.getppid()), seed=SEED, sites=args.sites, device=local)
     t_gen = time.perf_counter() - t_gen
     P_total = inst.patterns
     from paper_1905_12146_b200 import _lib as _L

@@ -215,6 +215,24 @@ int pg_compress_result_gpu(void* handle, int8_t* pattern_codes, int64_t* weights
                            float* device_ms);
 void pg_compress_free_gpu(void* handle);
 
+/* alignment.hpp:243-286 forward simulation on the GPU:
+ * per site the rate category, then the nodes in pre-order (the reverse of
+ * post_order, tree.hpp:76) -- the root from pi, the rest from the row of
+ * P(b_node c_l) of the parent's state (substitution.hpp:147-160) -- then a
+ * missing tip (-1) with probability gap_fraction per (taxon, site).  The
+ * reference draws from one sequential mt19937_64 stream; here draw k of site
+ * s is splitmix64 at counter s (3N-1+1) + k of `seed`, so sites are
+ * independent (one thread each) and the result is bit-identical with the
+ * CPU twin in workloads/ (PGW_SIM_COUNTER).  states: [tip_count][sites] int8
+ * in host memory, or in device memory on `device` when states_on_device != 0
+ * (e.g. straight into pg_compress_codes_gpu).  device_ms (may be NULL): the
+ * simulation kernel's time. */
+int pg_simulate_states_gpu(int tip_count, const int32_t* parent, const int32_t* post_order, int state_count,
+                           const double* q, const double* pi, int reversible, int category_count,
+                           const double* cat_rates, const double* cat_probs, const double* branch_lengths,
+                           int64_t sites, uint64_t seed, double gap_fraction, int device, int8_t* states,
+                           int states_on_device, float* device_ms);
+
 /* substitution.hpp:55-68 discrete_gamma_categories (bin medians, mean one). */
 int pg_discrete_gamma(double alpha, int count, double* rates, double* probs);
 

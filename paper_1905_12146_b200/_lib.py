@@ -42,7 +42,7 @@ EXPORTS = [
     "pg_timing", "pg_engine_variant",
     "pg_create_multi", "pg_group_info", "pg_clock_gradient",
     "pg_newick_parse", "pg_compress_codes", "pg_compress_result", "pg_compress_free", "pg_compress_codes_gpu",
-    "pg_compress_result_gpu", "pg_compress_free_gpu", "pg_discrete_gamma",
+    "pg_compress_result_gpu", "pg_compress_free_gpu", "pg_simulate_states_gpu", "pg_discrete_gamma",
 ]
 
 
@@ -170,6 +170,8 @@ def _declare(L):
         "pg_compress_codes_gpu": (I, [I, C.c_int64, P, I, I, I, C.POINTER(P), C.POINTER(I)]),
         "pg_compress_result_gpu": (I, [P, P, PI64, PI32, C.POINTER(C.c_float)]),
         "pg_compress_free_gpu": (None, [P]),
+        "pg_simulate_states_gpu": (I, [I, PI32, PI32, I, PD, PD, I, I, PD, PD, PD, C.c_int64, C.c_uint64, D, I, P, I,
+                                       C.POINTER(C.c_float)]),
         "pg_discrete_gamma": (I, [D, I, PD, PD]),
     }
     for name, (res, args) in sig.items():

@@ -76,4 +76,17 @@ RowMat expm_host(const RowMat& a, int n);
 double regularized_gamma_p(double a, double x);
 double gamma_quantile(double shape, double rate, double p);
 
+// Host P(t) = e^{Q t} for simulation (substitution.hpp:147-160: t = 0 -> I,
+// symmetric eigensystem for reversible models with pi > 0, Pade otherwise,
+// clamp >= 0).  One implementation for the CPU simulators (workloads/) and
+// the GPU simulator's transition tables (pg_simulate.cu), so both see
+// bit-identical cumulative rows.
+struct HostTransition {
+  int m = 0;
+  bool eig = false;
+  std::vector<double> w, U, Ui, q;
+  HostTransition(int m_, const std::vector<double>& q_, const std::vector<double>& pi_, int reversible);
+  std::vector<double> operator()(double t) const;
+};
+
 }  // namespace pg

@@ -169,4 +169,49 @@ double gamma_quantile(double shape, double rate, double p) {
 }
 
 
+HostTransition::HostTransition(int m_, const std::vector<double>& q_, const std::vector<double>& pi_, int reversible)
+    : m(m_), q(q_) {
+  bool pos = true;
+  for (double p : pi_) pos = pos && p > 0;
+  if (reversible && pos) {
+    std::vector<double> sym(static_cast<size_t>(m) * m), sp(static_cast<size_t>(m));
+    for (int i = 0; i < m; ++i) sp[size_t(i)] = std::sqrt(pi_[size_t(i)]);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j)
+        sym[size_t(i) * m + j] = 0.5 * (sp[size_t(i)] * q[size_t(i) * m + j] / sp[size_t(j)] +
+                                        sp[size_t(j)] * q[size_t(j) * m + i] / sp[size_t(i)]);
+    RowMat V;
+    symmetric_eigen(sym, m, w, V);
+    U.resize(size_t(m) * m);
+    Ui.resize(size_t(m) * m);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        U[size_t(i) * m + j] = V[size_t(i) * m + j] / sp[size_t(i)];
+        Ui[size_t(i) * m + j] = V[size_t(j) * m + i] * sp[size_t(j)];
+      }
+    eig = true;
+  }
+}
+
+std::vector<double> HostTransition::operator()(double t) const {
+  std::vector<double> p(size_t(m) * m, 0.0);
+  if (t == 0.0) {
+    for (int i = 0; i < m; ++i) p[size_t(i) * m + i] = 1.0;
+    return p;
+  }
+  if (eig) {
+    for (int i = 0; i < m; ++i)
+      for (int k = 0; k < m; ++k) {
+        const double u = U[size_t(i) * m + k] * std::exp(w[size_t(k)] * t);
+        for (int j = 0; j < m; ++j) p[size_t(i) * m + j] += u * Ui[size_t(k) * m + j];
+      }
+  } else {
+    RowMat a(q);
+    for (double& x : a) x *= t;
+    p = expm_host(a, m);
+  }
+  for (double& x : p) x = std::max(x, 0.0);
+  return p;
+}
+
 }  // namespace pg

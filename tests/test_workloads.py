@@ -69,3 +69,32 @@ def test_generator_does_not_map_the_product_library():
             "assert 'libpg_workloads.so' in maps\n"
             "assert 'libphylograd_b200' not in maps, 'product library mapped'\n") % ROOT
     subprocess.check_call([sys.executable, "-c", code])
+
+
+def test_counter_simulation_independent_of_threads_and_compressed_consistently():
+    """C3-C5 use the counter-based per-site stream (pg_simulate.hpp): the
+    columns do not depend on the thread count, and the instance's patterns are
+    the first-occurrence compression of exactly those columns."""
+    inst = synth.generate("C3", seed=21, sites=3000, tips=40, threads=1)
+    cols1 = synth.simulate_states_counter(inst.tip_count, inst.parent, inst.post_order, inst.q, inst.pi,
+                                          inst.reversible, inst.cat_rates, inst.cat_probs, inst.branch_lengths, 3000,
+                                          21, threads=1)
+    cols7 = synth.simulate_states_counter(inst.tip_count, inst.parent, inst.post_order, inst.q, inst.pi,
+                                          inst.reversible, inst.cat_rates, inst.cat_probs, inst.branch_lengths, 3000,
+                                          21, threads=7)
+    assert np.array_equal(cols1, cols7)
+    aln = O.Alignment.from_codes(cols1.astype(np.int32), inst.states)
+    assert np.array_equal(aln.pattern_codes(), inst.codes.astype(np.int32))
+    assert np.array_equal(aln.weights, inst.weights)
+    assert synth.CONFIGS["C3"]["sim"] == synth.SIM_COUNTER
+
+
+def test_counter_simulation_gaps_and_states():
+    inst = synth.generate("C4", seed=3, sites=100, tips=12)
+    cols = synth.simulate_states_counter(inst.tip_count, inst.parent, inst.post_order, inst.q, inst.pi, True,
+                                         inst.cat_rates, inst.cat_probs, inst.branch_lengths, 20000, 9, gap=0.05)
+    assert cols.min() == -1 and cols.max() <= 19
+    assert 0.04 < (cols < 0).mean() < 0.06
+    with pytest.raises(ValueError, match="gap fraction"):
+        synth.simulate_states_counter(inst.tip_count, inst.parent, inst.post_order, inst.q, inst.pi, True,
+                                      inst.cat_rates, inst.cat_probs, inst.branch_lengths, 10, 9, gap=1.5)

@@ -15,6 +15,7 @@
 
 #include "../paper_1905_12146_b200/csrc/pg_common.hpp"
 #include "../paper_1905_12146_b200/csrc/pg_hostutil.hpp"
+#include "../paper_1905_12146_b200/csrc/pg_simulate.hpp"
 #include "pg_workloads.h"
 
 #define PGW_API __attribute__((visibility("default")))
@@ -242,55 +243,11 @@ void draw_model(Synth& S, std::mt19937_64& rng) {
   }
 }
 
-// Host P(t) for simulation: eigen path for reversible models, Pade otherwise.
-struct HostP {
-  int m;
-  bool eig = false;
-  std::vector<double> w, U, Ui;
-  std::vector<double> q;
-  HostP(const Synth& S) : HostP(S.m, S.q, S.pi, S.reversible) {}
-  HostP(int m_, const std::vector<double>& q_, const std::vector<double>& pi_, int reversible) : m(m_), q(q_) {
-    bool pos = true;
-    for (double p : pi_) pos = pos && p > 0;
-    if (reversible && pos) {
-      std::vector<double> sym(static_cast<size_t>(m) * m), sp(static_cast<size_t>(m));
-      for (int i = 0; i < m; ++i) sp[size_t(i)] = std::sqrt(pi_[size_t(i)]);
-      for (int i = 0; i < m; ++i)
-        for (int j = 0; j < m; ++j)
-          sym[size_t(i) * m + j] = 0.5 * (sp[size_t(i)] * q[size_t(i) * m + j] / sp[size_t(j)] +
-                                          sp[size_t(j)] * q[size_t(j) * m + i] / sp[size_t(i)]);
-      RowMat V;
-      symmetric_eigen(sym, m, w, V);
-      U.resize(size_t(m) * m);
-      Ui.resize(size_t(m) * m);
-      for (int i = 0; i < m; ++i)
-        for (int j = 0; j < m; ++j) {
-          U[size_t(i) * m + j] = V[size_t(i) * m + j] / sp[size_t(i)];
-          Ui[size_t(i) * m + j] = V[size_t(j) * m + i] * sp[size_t(j)];
-        }
-      eig = true;
-    }
-  }
-  std::vector<double> operator()(double t) const {
-    std::vector<double> p(size_t(m) * m, 0.0);
-    if (t == 0.0) {
-      for (int i = 0; i < m; ++i) p[size_t(i) * m + i] = 1.0;
-      return p;
-    }
-    if (eig) {
-      for (int i = 0; i < m; ++i)
-        for (int k = 0; k < m; ++k) {
-          const double u = U[size_t(i) * m + k] * std::exp(w[size_t(k)] * t);
-          for (int j = 0; j < m; ++j) p[size_t(i) * m + j] += u * Ui[size_t(k) * m + j];
-        }
-    } else {
-      RowMat a(q);
-      for (double& x : a) x *= t;
-      p = expm_host(a, m);
-    }
-    for (double& x : p) x = std::max(x, 0.0);
-    return p;
-  }
+// Host P(t) for simulation (pg_linalg.cpp): shared with the GPU simulator.
+struct HostP : HostTransition {
+  explicit HostP(const Synth& S) : HostTransition(S.m, S.q, S.pi, S.reversible) {}
+  HostP(int m_, const std::vector<double>& q_, const std::vector<double>& pi_, int reversible)
+      : HostTransition(m_, q_, pi_, reversible) {}
 };
 
 void simulate_blocked(Synth& S);
@@ -349,7 +306,45 @@ void simulate_reference(int N, const int32_t* parent, const int32_t* post, int m
   }
 }
 
+// Counter-based per-site stream (pg_simulate.hpp): the CPU twin of
+// pg_simulate_states_gpu.  out: [N][sites].
+void simulate_counter(int N, const int32_t* parent, const int32_t* post, int m, const HostTransition& P, int L,
+                      const double* cat_rates, const double* cat_probs, const double* pi, const double* blen,
+                      int64_t sites, uint64_t seed, double gap, int threads, int8_t* out) {
+  const int n = 2 * N - 1;
+  std::vector<double> cdf, root, cat;
+  build_sim_tables(N, m, L, P, cat_rates, cat_probs, pi, blen, cdf, root, cat);
+  const uint64_t D = sim::draws_per_site(N);
+  parallel_for(sites, hw_threads(threads), [&](int64_t a, int64_t b) {
+    std::vector<int> state(size_t(n + 1), 0);
+    for (int64_t s = a; s < b; ++s) {
+      const int l = sim::pick(cat.data(), L, sim::unit(seed, uint64_t(s), D, 0));
+      for (int j = 0; j < n; ++j) {
+        const int v = post[n - 1 - j];
+        const double u = sim::unit(seed, uint64_t(s), D, uint64_t(1 + j));
+        state[size_t(v)] = v == n ? sim::pick(root.data(), m, u)
+                                  : sim::pick(&cdf[((size_t(v) * L + l) * m + size_t(state[size_t(parent[v])])) * m], m, u);
+        if (v <= N) out[size_t(v - 1) * size_t(sites) + size_t(s)] = int8_t(state[size_t(v)]);
+      }
+      if (gap > 0.0)
+        for (int t = 0; t < N; ++t)
+          if (sim::unit(seed, uint64_t(s), D, uint64_t(1 + n + t)) < gap) out[size_t(t) * size_t(sites) + size_t(s)] = -1;
+    }
+  });
+}
+
 void simulate(Synth& S) {
+  if (S.spec.sim == PGW_SIM_NONE) return;
+  if (S.spec.sim == PGW_SIM_COUNTER) {
+    const int N = S.N, T = hw_threads(S.spec.threads);
+    const int64_t sites = S.spec.sites;
+    HostP hp(S);
+    std::vector<int8_t> codes(size_t(N) * size_t(sites));
+    simulate_counter(N, S.parent.data(), S.post.data(), S.m, hp, S.L, S.cat_rates.data(), S.cat_probs.data(),
+                     S.pi.data(), S.blen.data(), sites, S.spec.seed, S.spec.gap_fraction, T, codes.data());
+    compress_into(S, codes, T);
+    return;
+  }
   if (S.spec.sim == PGW_SIM_REFERENCE) {
     const int N = S.N, T = hw_threads(S.spec.threads);
     const int64_t sites = S.spec.sites;
@@ -534,6 +529,25 @@ PGW_API int pgw_simulate_states(int tip_count, const int32_t* parent, const int3
     HostP hp(m, std::vector<double>(q, q + size_t(m) * m), std::vector<double>(pi, pi + m), reversible);
     simulate_reference(tip_count, parent, post_order, m, hp, category_count, cat_rates, cat_probs, pi,
                        branch_lengths, sites, seed, states);
+  });
+}
+
+PGW_API int pgw_simulate_states_counter(int tip_count, const int32_t* parent, const int32_t* post_order,
+                                        int state_count, const double* q, const double* pi, int reversible,
+                                        int category_count, const double* cat_rates, const double* cat_probs,
+                                        const double* branch_lengths, int64_t sites, uint64_t seed,
+                                        double gap_fraction, int threads, int8_t* states) {
+  return guarded([&] {
+    if (sites < 1) throw std::invalid_argument("simulate: site_count must be >= 1");
+    if (tip_count < 2 || state_count < 2 || state_count > 127 || category_count < 1)
+      throw std::invalid_argument("simulate: bad sizes");
+    if (!(gap_fraction >= 0.0 && gap_fraction < 1.0)) throw std::invalid_argument("simulate: gap fraction in [0, 1)");
+    for (int i = 0; i < 2 * tip_count - 2; ++i)
+      if (!(branch_lengths[i] >= 0.0)) throw std::invalid_argument("transition matrix: negative branch length");
+    const int m = state_count;
+    HostTransition P(m, std::vector<double>(q, q + size_t(m) * m), std::vector<double>(pi, pi + m), reversible);
+    simulate_counter(tip_count, parent, post_order, m, P, category_count, cat_rates, cat_probs, pi, branch_lengths,
+                     sites, seed, gap_fraction, threads, states);
   });
 }
 

@@ -15,10 +15,12 @@
  *    cumulative scan of alignment.hpp:258-266.  Sequential; used for the
  *    small configs (C1, C2) so the reference's own simulate_states
  *    regenerates them.
+ *  - PGW_SIM_COUNTER: a counter-based per-site stream (draw k of site s =
+ *    splitmix64 at counter s D + k of the seed; pg_simulate.hpp), the CPU
+ *    twin of the product's GPU simulator pg_simulate_states_gpu (bit-identical
+ *    columns).  Used for the 10^5..10^6-column configs (C3-C5).
  *  - PGW_SIM_BLOCKED: independent mt19937_64 streams per block of 4096 sites
- *    (seeded from seed and the block index), so the 10^5..10^6-column configs
- *    (C3-C5) simulate on every host core; output does not depend on the
- *    thread count.
+ *    (round-1 workloads; kept for reproducing them).
  */
 #ifndef PG_WORKLOADS_H
 #define PG_WORKLOADS_H
@@ -29,7 +31,9 @@
 extern "C" {
 #endif
 
-enum pgw_sim { PGW_SIM_BLOCKED = 0, PGW_SIM_REFERENCE = 1 };
+/* PGW_SIM_NONE: tree, model and lengths only (no columns; e.g. to simulate
+ * them on the GPU with pg_simulate_states_gpu from the same seed). */
+enum pgw_sim { PGW_SIM_BLOCKED = 0, PGW_SIM_REFERENCE = 1, PGW_SIM_COUNTER = 2, PGW_SIM_NONE = 3 };
 
 typedef struct pgw_spec {
   int tips;
@@ -69,6 +73,14 @@ int pgw_simulate_states(int tip_count, const int32_t* parent, const int32_t* pos
                         const double* q, const double* pi, int reversible, int category_count,
                         const double* cat_rates, const double* cat_probs, const double* branch_lengths,
                         int64_t sites, uint64_t seed, int8_t* states);
+
+/* The counter-based simulation (PGW_SIM_COUNTER) of raw columns, host side:
+ * the same arguments and result as pg_simulate_states_gpu (tip states
+ * [tip_count][sites] int8, -1 gap); threads 0 = all cores. */
+int pgw_simulate_states_counter(int tip_count, const int32_t* parent, const int32_t* post_order, int state_count,
+                                const double* q, const double* pi, int reversible, int category_count,
+                                const double* cat_rates, const double* cat_probs, const double* branch_lengths,
+                                int64_t sites, uint64_t seed, double gap_fraction, int threads, int8_t* states);
 
 #ifdef __cplusplus
 }

@@ -6,8 +6,10 @@ numbered like parse_newick, model parameters drawn as the config states,
 forward simulation down the tree (alignment.hpp:243-286), optional gaps, then
 first-occurrence pattern compression.  C1 and C2 are simulated in the
 reference's own draw order (one mt19937_64 stream, so the reference's
-simulate_states regenerates their columns); C3-C5 (10^5..10^6 columns) use
-independent per-block streams so they simulate on every host core.
+simulate_states regenerates their columns); C3-C5 (10^5..10^6 columns) use a
+counter-based per-site stream (pg_simulate.hpp) so they simulate in parallel:
+on every host core here, or on the GPU with the product's
+pg_simulate_states_gpu (`generate(..., device=d)`), with identical columns.
 
 Input generation only — never inside a timed region.  The native code is
 workloads/_build/libpg_workloads.so, a host library separate from the product
@@ -25,7 +27,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "_build", "libpg_workloads.so")
-SIM_BLOCKED, SIM_REFERENCE = 0, 1
+SIM_BLOCKED, SIM_REFERENCE, SIM_COUNTER, SIM_NONE = 0, 1, 2, 3
 
 
 class Spec(C.Structure):
@@ -67,6 +69,8 @@ def lib():
             "pgw_free": (None, [_P]),
             "pgw_simulate_states": (_I, [_I, _PI32, _PI32, _I, _PD, _PD, _I, _I, _PD, _PD, _PD, C.c_int64,
                                          C.c_uint64, _PI8]),
+            "pgw_simulate_states_counter": (_I, [_I, _PI32, _PI32, _I, _PD, _PD, _I, _I, _PD, _PD, _PD, C.c_int64,
+                                                 C.c_uint64, _D, _I, _PI8]),
         }.items():
             f = getattr(L, name)
             f.restype = res
@@ -90,9 +94,11 @@ CONFIGS = {
     "C2": dict(tips=512, model_kind=1, categories=4, gamma_alpha=0.5, sites=20000, branch_mean=0.01,
                gap_fraction=0.02, sim=SIM_REFERENCE),
     "C3": dict(tips=2048, model_kind=2, categories=4, gamma_alpha=0.5, sites=1000000, clock=1, dt_mean=5.0,
-               rate_scale=1e-3, rate_sd=0.3),
-    "C4": dict(tips=1000, model_kind=3, categories=4, gamma_alpha=0.5, sites=200000, branch_mean=0.05),
-    "C5": dict(tips=256, model_kind=4, categories=4, gamma_alpha=0.5, sites=400000, branch_mean=0.1),
+               rate_scale=1e-3, rate_sd=0.3, sim=SIM_COUNTER),
+    "C4": dict(tips=1000, model_kind=3, categories=4, gamma_alpha=0.5, sites=200000, branch_mean=0.05,
+               sim=SIM_COUNTER),
+    "C5": dict(tips=256, model_kind=4, categories=4, gamma_alpha=0.5, sites=400000, branch_mean=0.1,
+               sim=SIM_COUNTER),
 }
 DESCRIPTIONS = {
     "C1": "HKY85 k=2 pi=(.3,.2,.2,.3), L=1, Yule-64, b~Exp(0.02), 1000 columns",
@@ -157,7 +163,10 @@ class Instance:
 
 
 def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int | None = None,
-             threads: int = 0, sim: int | None = None) -> Instance:
+             threads: int = 0, sim: int | None = None, device: int | None = None) -> Instance:
+    """A seeded BASELINE.json workload.  device: simulate and compress the
+    columns on that GPU (counter-stream configs only; loads the product
+    library) -- the same Instance as the host path."""
     cfg = dict(CONFIGS[name])
     spec = Spec()
     spec.tips = tips or cfg["tips"]
@@ -174,6 +183,9 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
     spec.seed = seed
     spec.threads = threads
     spec.sim = cfg.get("sim", SIM_BLOCKED) if sim is None else sim
+    on_gpu = device is not None and spec.sim == SIM_COUNTER
+    if on_gpu:
+        spec.sim = SIM_NONE
     L = lib()
     h = C.c_void_p()
     P = C.c_int()
@@ -198,9 +210,13 @@ def generate(name: str, seed: int = 12146, sites: int | None = None, tips: int |
         cp = np.zeros(spec.categories)
         check(L.pgw_model(h, ptr(q, C.c_double), ptr(pi, C.c_double), C.byref(rev), ptr(cr, C.c_double),
                                ptr(cp, C.c_double)))
-        codes = np.zeros((N, P.value), np.int8)
-        w = np.zeros(P.value, np.int64)
-        check(L.pgw_patterns(h, ptr(codes, C.c_int8), ptr(w, C.c_int64)))
+        if on_gpu:
+            codes, w = _columns_on_gpu(N, parent, post, q.reshape(mm, mm), pi, rev.value, cr, cp, blen, spec.sites,
+                                       seed, spec.gap_fraction, device)
+        else:
+            codes = np.zeros((N, P.value), np.int8)
+            w = np.zeros(P.value, np.int64)
+            check(L.pgw_patterns(h, ptr(codes, C.c_int8), ptr(w, C.c_int64)))
     finally:
         L.pgw_free(h)
     return Instance(name, N, parent, children.reshape(n + 1, 2), post, blen, dt, rr, q.reshape(mm, mm), pi,
@@ -228,7 +244,7 @@ def tips_of(cfg) -> int:
 
 
 def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: int = 12146,
-                    sites: int | None = None) -> Instance:
+                    sites: int | None = None, device: int | None = None) -> Instance:
     """One rank of a node simulates the workload with every host core and
     shares it through node-local shared memory; the other ranks load it
     (identical input everywhere; each rank then keeps its pattern shard).
@@ -236,7 +252,7 @@ def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: i
     import os
 
     if world <= 1:
-        return generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1)
+        return generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1, device=device)
     # node-local shared memory when it has room for the codes (N x sites
     # bytes plus the small arrays), else /tmp
     cfg = CONFIGS[name]
@@ -248,13 +264,65 @@ def generate_shared(name: str, rank: int, world: int, barrier, tag: str, seed: i
             shm = "/dev/shm"
     path = os.path.join(shm, f"pg_synth_{name}_{seed}_{sites or 0}_{tag}.npz")
     if rank == 0:
-        generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1).save(path)
+        generate(name, seed=seed, sites=sites, threads=os.cpu_count() or 1, device=device).save(path)
     barrier()
     inst = Instance.load(path)
     barrier()
     if rank == 0:
         os.remove(path)
     return inst
+
+
+def _columns_on_gpu(N, parent, post, q, pi, reversible, cat_rates, cat_probs, blen, sites, seed, gap, device):
+    """pg_simulate_states_gpu into device memory, then pg_compress_codes_gpu
+    on the device-resident columns: (pattern codes [N][P] int8, weights)."""
+    import torch
+
+    from paper_1905_12146_b200 import _lib as PL
+
+    L = PL.lib()
+    m = int(q.shape[0])
+    cols = torch.empty((N, sites), dtype=torch.int8, device=f"cuda:{device}")
+    f = C.c_float()
+    qq = np.ascontiguousarray(q, np.float64)
+    PL.check(L.pg_simulate_states_gpu(N, ptr(np.ascontiguousarray(parent, np.int32), C.c_int32),
+                                      ptr(np.ascontiguousarray(post, np.int32), C.c_int32), m, ptr(qq, C.c_double),
+                                      ptr(np.ascontiguousarray(pi, np.float64), C.c_double), int(reversible),
+                                      len(cat_rates), ptr(np.ascontiguousarray(cat_rates, np.float64), C.c_double),
+                                      ptr(np.ascontiguousarray(cat_probs, np.float64), C.c_double),
+                                      ptr(np.ascontiguousarray(blen, np.float64), C.c_double), sites, seed, gap, device,
+                                      cols.data_ptr(), 1, C.byref(f)))
+    h = C.c_void_p()
+    P = C.c_int()
+    PL.check(L.pg_compress_codes_gpu(N, sites, cols.data_ptr(), 1, m, device, C.byref(h), C.byref(P)))
+    try:
+        codes = np.zeros((N, P.value), np.int8)
+        w = np.zeros(P.value, np.int64)
+        PL.check(L.pg_compress_result_gpu(h, codes.ctypes.data_as(C.c_void_p), ptr(w, C.c_int64), None, None))
+    finally:
+        L.pg_compress_free_gpu(h)
+    del cols
+    return codes, w
+
+
+def simulate_states_counter(tip_count, parent, post_order, q, pi, reversible, cat_rates, cat_probs, branch_lengths,
+                            sites, seed, gap=0.0, threads=0):
+    """The counter-based per-site simulation (host twin of
+    pg_simulate_states_gpu): tip states [tip_count][sites] int8, -1 gap."""
+    m = int(np.asarray(q).shape[0])
+    out = np.zeros((tip_count, sites), np.int8)
+    q = np.ascontiguousarray(q, np.float64)
+    pi = np.ascontiguousarray(pi, np.float64)
+    cr = np.ascontiguousarray(cat_rates, np.float64)
+    cp = np.ascontiguousarray(cat_probs, np.float64)
+    b = np.ascontiguousarray(branch_lengths, np.float64)
+    par = np.ascontiguousarray(parent, np.int32)
+    post = np.ascontiguousarray(post_order, np.int32)
+    check(lib().pgw_simulate_states_counter(tip_count, ptr(par, C.c_int32), ptr(post, C.c_int32), m,
+                                            ptr(q, C.c_double), ptr(pi, C.c_double), int(bool(reversible)), len(cr),
+                                            ptr(cr, C.c_double), ptr(cp, C.c_double), ptr(b, C.c_double), sites, seed,
+                                            float(gap), threads, ptr(out, C.c_int8)))
+    return out
 
 
 def simulate_states(tip_count, parent, post_order, q, pi, reversible, cat_rates, cat_probs, branch_lengths,
