@@ -21,7 +21,6 @@
 #include "pg_common.hpp"
 #include "pg_kernels.cuh"
 #include "pg_walk.cuh"
-#include "pg_walk4x_tables.hpp"
 #include "pg_walkl.cuh"
 
 void* pg_walk4_kernel_lc4(bool homog, bool hess, int nc);
@@ -33,7 +32,6 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
 }
 int pg_walk4_nc(int nc);
-void* pg_walk4x_kernel(bool homog, bool hess, int nc, int L, size_t* smem);
 void* pg_walkl_kernel(int L, bool homog, bool hess);
 void* pg_walkm_kernel(int mp, bool hess);
 size_t pg_walkm_smem(int mp);
@@ -135,7 +133,6 @@ struct pg_engine {
   // geometry
   int MP = 0, LC = 0, G = 0, NC = 0, TW = 0, ntiles = 0, accw = 0;
   bool use_walk4 = false;
-  bool use_walk4x = false;  // category-parallel 4-state walk (pg_walk4x.cuh): one CTA of L warps per tile
   bool use_walkl = false;   // level-scheduled 4-state traversal (pg_walkl.cuh): small P
   // P up to this x SMs: level-scheduled (PG_WALKL=0/1 forces).  Measured on C2
   // (512 taxa, GTR+G4): 1,250 patterns 0.30 vs 1.83 ms, 2,500 0.43 vs 2.37 ms,
@@ -157,8 +154,6 @@ struct pg_engine {
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err;
   DevBuf<int4> d_post, d_pre;
-  DevBuf<pgk::Walk4xHdr> d_xhdr;   // walk4x step headers (post, then pre)
-  DevBuf<pgk::Walk4xCopy> d_xcpy;  // walk4x per-step copy lists
   DevBuf<double> d_escr, d_qscr, d_acc, d_out, d_site_ll;
   DevBuf<double> d_cap_post, d_cap_pre;
   DevBuf<int> d_cap_post_exp, d_cap_pre_exp;
@@ -633,20 +628,8 @@ struct pg_engine {
       G = L / walk4_lcv;
       ntiles = (P + 32 / G - 1) / (32 / G);
       const size_t tcb = size_t(L) * NC * 4;
-      // category-parallel, warp-specialised variant (pg_walk4x.cuh): opt-in
-      // with PG_WALK4X=1 -- measured slower than walk4 on C2 / C3 (C3 250 vs
-      // 152 ms: the per-step control work is repeated by every category warp,
-      // 1.8x the instructions)
-      const char* wx = std::getenv("PG_WALK4X");
-      use_walk4x = (wx != nullptr && std::atoi(wx) != 0) &&
-                   pg_walk4x_kernel(branch_q.empty(), false, NC, L, &walk_smem) != nullptr;
-      if (use_walk4x) {
-        G = 1;
-        ntiles = (P + 31) / 32;
-      } else {
-        walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
-                    sizeof(double2);
-      }
+      walk_smem = size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
+                  sizeof(double2);
     }
     if (use_walkl) {
       G = L;
@@ -654,17 +637,16 @@ struct pg_engine {
       build_levels();
     }
     if (use_walkm) {
-      use_walk4 = use_walk4x = use_walkl = false;
+      use_walk4 = use_walkl = false;
       LC = 1;
       G = 4;  // a quad of lanes per pattern (DMMA fragment layout)
       walkm_wpc = pg_walkm_wpc(MP);
       ntiles = (P + 8 * walkm_wpc - 1) / (8 * walkm_wpc);  // CTA tiles of 8 patterns per warp
       walk_smem = pg_walkm_smem(MP);
     }
-    const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : use_walk4x ? 1 : pgk::kWarpsPerBlock);
+    const int maxw = walk_max_blocks_per_sm() * num_sms * (use_walkm ? walkm_wpc : pgk::kWarpsPerBlock);
     // walkm slot per (node, category): 8 patterns x MP doubles + 8 int exponents;
-    // walk4x: one CTA tile's slot (L categories x 32 patterns x 4 states)
-    const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : use_walk4x ? size_t(L) * 32 * 4 : size_t(32) * LC * MP;
+    const size_t vec = use_walkm ? size_t(L) * (8 * MP + 4) : size_t(32) * LC * MP;
     if (use_walkl) {
       // every internal node's e and q for all patterns; one accumulator row per tile
       TW = ntiles;
@@ -699,8 +681,6 @@ struct pg_engine {
       // CTA tiles: 4 warps per tile
       int ctas = std::max(1, std::min({maxw / walkm_wpc, std::max(ntiles, 1), std::max(cap / walkm_wpc, 1)}));
       TW = ctas * walkm_wpc;
-    } else if (use_walk4x) {
-      TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));  // CTAs (one accumulator row each)
     } else {
       TW = std::max(1, std::min({maxw, std::max(ntiles, 1), cap}));
       TW = (TW + pgk::kWarpsPerBlock - 1) / pgk::kWarpsPerBlock * pgk::kWarpsPerBlock;
@@ -723,13 +703,6 @@ struct pg_engine {
       d_fpt.ensure(size_t(B()) * L * frag);
     }
     d_post.upload(post_steps.data(), post_steps.size(), stream);
-    if (use_walk4x) {
-      std::vector<pgk::Walk4xHdr> xh;
-      std::vector<pgk::Walk4xCopy> xc;
-      pgk::build_walk4x_tables(post_steps, pre_steps, N, L, NC, Pc, xh, xc);
-      d_xhdr.upload(xh.data(), xh.size(), stream);
-      d_xcpy.upload(xc.data(), xc.size(), stream);
-    }
     d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
     if (!h_out) {
       PG_CUDA(cudaMallocHost(&h_err, 3 * sizeof(int)));
@@ -959,17 +932,6 @@ int pg_engine::walk_max_blocks_per_sm() {
     }
     return std::max(nb, 1);
   }
-  if (use_walk4x) {
-    for (int v = 0; v < 2; ++v) {
-      size_t sm = 0;
-      const void* fn = pg_walk4x_kernel(branch_q.empty(), v & 1, NC, L, &sm);
-      PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      int b = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * (L + 1), sm));
-      nb = v == 0 ? b : std::min(nb, b);
-    }
-    return std::max(nb, 1);
-  }
   if (use_walk4) {
     // occupancy of the model's variants (with and without the Hessian) bounds the grid
     for (int v = 0; v < 2; ++v) {
@@ -1095,17 +1057,6 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     for (int i = 0; i < 4; ++i) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
-    }
-    if (use_walk4x) {
-      size_t sm = 0;
-      void* fx = pg_walk4x_kernel(branch_q.empty(), do_hess, NC, L, &sm);
-      pgk::Walk4xParams px{};
-      px.p4 = p4;
-      px.hdr = d_xhdr.p;
-      px.cpy = d_xcpy.p;
-      void* args[] = {&px};
-      PG_CUDA(cudaLaunchKernel(fx, dim3(unsigned(TW)), dim3(32 * (L + 1)), args, sm, stream));
-      return;
     }
     void* fn = pg_walk4_kernel(branch_q.empty(), do_hess, NC, walk4_lcv, L);
     void* args[] = {&p4};
@@ -1622,7 +1573,7 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
 
 int pg_engine_variant(const pg_engine* e) {
   e = primary(e);
-  return e->use_walkm ? 2 : e->use_walk4x ? 3 : e->use_walkl ? 4 : e->use_walk4 ? 1 : 0;
+  return e->use_walkm ? 2 : e->use_walkl ? 3 : e->use_walk4 ? 1 : 0;
 }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {

@@ -1,11 +1,9 @@
-"""Direct oracle parity of every 4-state walk variant (the C2/C3 bench
+"""Direct oracle parity of every 4-state kernel variant (the C2/C3 bench
 kernels): the per-warp walk4_kernel<HOMOG, HESS, NC, LCV> with one lane per
-pattern (LCV=4) or two (LCV=2) forced through PG_WALK4_LCV, and the opt-in
-category-parallel walk4x_kernel<HOMOG, HESS, NC, L> (PG_WALK4X=1: warp l of
-a CTA holds category l of a 32-pattern tile, a producer warp stages);
-homogeneous and per-branch generators, with and without the Hessian, gaps
-only (NC=5) and IUPAC ambiguity classes (NC=16).  walk4x evaluates walk4's
-arithmetic chains in the same order, so the two agree bit for bit."""
+pattern (LCV=4) or two (LCV=2) forced through PG_WALK4_LCV, and the
+level-scheduled walkl_kernel<L, HOMOG, HESS> (PG_WALKL=1; the small-P
+default); homogeneous and per-branch generators, with and without the
+Hessian, gaps only (NC=5) and IUPAC ambiguity classes (NC=16)."""
 import numpy as np
 import pytest
 
@@ -20,17 +18,13 @@ from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCate
                                        SitePatternAlignment, SubstitutionModel, Tree, parse_fasta, parse_newick)
 
 
-@pytest.fixture(params=["cat", "lvl", 4, 2], ids=["walk4x", "walkl", "lcv4", "lcv2"])
+@pytest.fixture(params=["lvl", 4, 2], ids=["walkl", "lcv4", "lcv2"])
 def lcv(request, monkeypatch):
     """The kernel variant under test; returns (kernel name, lanes per pattern)."""
     if request.param == "lvl":
         monkeypatch.setenv("PG_WALKL", "1")
         return "walkl_kernel", 4
     monkeypatch.setenv("PG_WALKL", "0")
-    if request.param == "cat":
-        monkeypatch.setenv("PG_WALK4X", "1")
-        return "walk4x_kernel", 1
-    monkeypatch.setenv("PG_WALK4X", "0")
     monkeypatch.setenv("PG_WALK4_LCV", str(request.param))
     return "walk4_kernel", 4 // request.param
 
@@ -170,28 +164,6 @@ def test_walk4_other_category_counts(L, homog, level, monkeypatch):
         assert_vec(rep.branch_gradient, g)
         if hess:
             assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
-
-
-@pytest.mark.parametrize("name,sites,hess", [("C3", 40000, False), ("C3", 40000, True), ("C2", 12000, False)])
-def test_walk4x_matches_walk4(monkeypatch, name, sites, hess):
-    """walk4x (category-parallel) and walk4 (one lane per pattern) evaluate
-    the same per-pattern arithmetic chains; only the grouping of the
-    per-tile sums into accumulator rows differs (CTA rows vs warp rows), so
-    logL, gradient and Hessian agree to ~1e-13 relative."""
-    inst = synth.generate(name, sites=sites, tips=256)
-    monkeypatch.setenv("PG_WALK4_LCV", "4")
-    monkeypatch.setenv("PG_WALK4X", "0")
-    e4, _ = _instance_pair(inst)
-    r4 = e4.branch_gradient(hess)
-    assert e4.info()["kernel"] == "walk4_kernel"
-    monkeypatch.setenv("PG_WALK4X", "1")
-    ex, _ = _instance_pair(inst)
-    rx = ex.branch_gradient(hess)
-    assert ex.info()["kernel"] == "walk4x_kernel"
-    assert_logl(rx.log_likelihood, r4.log_likelihood, rtol=1e-13)
-    assert_vec(rx.branch_gradient, r4.branch_gradient, rtol=1e-12)
-    if hess:
-        assert_vec(rx.hessian_diagonal, r4.hessian_diagonal, rtol=1e-11, what="hessian")
 
 
 @pytest.mark.parametrize("sites", [2500, 600])
