@@ -30,8 +30,8 @@ def _fixture(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,kernel,lanes", [("C3", "walk4_kernel", 1), ("C4", "walkm_kernel", 4),
-                                               ("C5", "walkm_kernel", 4)])
+@pytest.mark.parametrize("name,kernel,lanes", [("C2", "walk4_kernel", 2), ("C3", "walk4_kernel", 1),
+                                               ("C4", "walkm_kernel", 4), ("C5", "walkm_kernel", 4)])
 def test_full_size_workload_matches_oracle(name, kernel, lanes):
     fx = _fixture(name)
     inst = synth.generate(name, seed=SEED, threads=os.cpu_count() or 1)

@@ -490,3 +490,29 @@ def test_brute_force_fig1_bracketed_sum():  # test_validation.cpp:11-32
         inner = sum(p(4, 0.05)[y5, y4] * p(1, 0.1)[y4, 0] * p(2, 0.2)[y4, 1] for y4 in range(4))
         total += model.pi[y5] * inner * p(3, 0.3)[y5, 2]
     assert abs(v - math.log(total)) < 1e-14
+
+
+@pytest.mark.parametrize("name,sites", [("C4", 4000), ("C5", 2000)])
+def test_oracle_p_method_spread(name, sites):
+    """The fp64 uncertainty the parity bar must allow for: the reference
+    computes P(t) by a symmetric eigensystem for reversible models and by
+    Pade scaling-and-squaring otherwise (substitution.hpp:153-156).  Running
+    the SAME reversible instance through both paths moves cancelling gradient
+    components by more than 1e-9 relative, but by < 1e-10 of each component's
+    condition (oracle gradient_condition) -- the condition-aware bound of
+    tests/helpers.py (COND_RTOL)."""
+    import dataclasses
+
+    from tests.helpers import COND_RTOL, oracle_for
+    from workloads import synth
+
+    inst = synth.generate(name, seed=12146, sites=sites)
+    a = oracle_for(inst, blocks=8)
+    lla, ga, _ = a.branch_gradient(False)
+    cond = a.gradient_condition()
+    b = oracle_for(dataclasses.replace(inst, reversible=False), blocks=8)
+    llb, gb, _ = b.branch_gradient(False)
+    err = np.abs(ga - gb)
+    assert abs(lla - llb) <= 1e-12 * abs(lla)
+    assert np.max(err / np.abs(ga)) > 1e-9        # the plain relative bar is below the method spread
+    assert np.max(err / cond) < COND_RTOL          # the condition-aware bar is above it
