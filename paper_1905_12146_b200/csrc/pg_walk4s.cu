@@ -1,0 +1,24 @@
+// Instantiations of the single-buffered 4-state walk (pg_walk4s.cuh): 4 rate
+// categories, one lane per pattern, homogeneous / per-branch generators x
+// with / without the Hessian x TC column counts NC in {5, 16}.
+#include "pg_walk4s.cuh"
+
+#define PG_W4S(H, S, NC) \
+  if (homog == H && hess == S && nc == NC) return reinterpret_cast<void*>(&pgk::walk4s_kernel<H, S, NC>);
+
+void* pg_walk4s_kernel(bool homog, bool hess, int nc) {
+  PG_W4S(true, false, 5)
+  PG_W4S(true, true, 5)
+  PG_W4S(false, false, 5)
+  PG_W4S(false, true, 5)
+  PG_W4S(true, false, 16)
+  PG_W4S(true, true, 16)
+  PG_W4S(false, false, 16)
+  PG_W4S(false, true, 16)
+  return nullptr;
+}
+
+size_t pg_walk4s_smem(int nc) {
+  const size_t warp = nc <= 5 ? pgk::Walk4SGeom<5>::WARP : pgk::Walk4SGeom<16>::WARP;
+  return size_t(pgk::kWarpsPerBlock) * warp * sizeof(double2);
+}

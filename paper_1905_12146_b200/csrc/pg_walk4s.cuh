@@ -1,0 +1,510 @@
+// K2a'' — the 4-state, 4-category walk (one lane = one pattern, 32 patterns
+// per warp tile, persistent warps) laid out for occupancy.
+//
+// walk4_kernel (pg_walk4.cuh) holds every vector of a step in registers (the
+// kept edge message, the normalised product, both outgoing pre-partials: 64
+// fp64 per lane) and double-buffers its shared-memory stage, so it runs at
+// 255 registers and 114 KB per 4-warp CTA: 8 warps per SM.  Its C3 profile
+// (profiles/r22_walk_C3_full_source.txt) is latency-bound -- fixed-latency and
+// shared-memory dependency stalls with two warps per scheduler, 39 % issue
+// utilisation, memory waits ~2 % -- so this variant trades the prefetch stage
+// for warps:
+//  * one shared-memory stage per warp: slots Q (the step's pre-partial, or
+//    the post-order edge message handed to the next step), A and B (the
+//    children's staged edge messages, or a tip child's Q P table), two TC
+//    blocks and the tip code rows (13.8 KB per warp);
+//  * results are written in place: a post-order step's edge message goes to
+//    slot Q category by category after that category's operands are read, a
+//    pre-order step's outgoing pre-partial for the child visited next
+//    likewise, the other one to its scratch slot -- no per-lane vector
+//    arrays survive the category loop of the pre-order pass;
+//  * the pre-partials' power-of-two normalisation is applied by the consumer
+//    (the producer knows the peak only after the last category): the scale
+//    of the handed-on one travels in a register, a deferred one's exponent
+//    is stored next to its scratch slot ([TW][N-1][32] ints) -- the same
+//    values as walk4_kernel's, multiplied at read instead of at write;
+//  * a step's loads are issued once the previous step has consumed its
+//    operands and waited on at the top of the step; latency is hidden by the
+//    other warps (up to 16 per SM), and the edge messages the pre-order pass
+//    reads from DRAM are prefetched into L2 `pf` steps ahead.
+// Arithmetic and operation order per value are walk4_kernel's, so results are
+// bit-identical to it.
+#pragma once
+
+#include "pg_walk4.cuh"
+
+#ifndef PG_WALK4S_MINB
+#define PG_WALK4S_MINB 4
+#endif
+
+namespace pgk {
+
+__device__ __forceinline__ void prefetch_l2(const void* gmem) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
+}
+
+template <int NC>
+struct Walk4SGeom {
+  static constexpr int MP = 4, L = 4;
+  static constexpr int TCB = L * NC * MP;  // doubles per node TC block
+  static constexpr int TCC = TCB / 2;      // double2 chunks per TC block
+  static constexpr int VEC = 32 * L * MP;  // doubles per node slot of one warp
+  static constexpr int SD2 = VEC / 2;      // double2 per node slot
+  // per warp: slots Q, A, B; TC blocks 0, 1; code rows (2 x 32 B); exponent row (32 ints)
+  static constexpr int WARP = 3 * SD2 + 2 * TCC + 4 + 8;  // double2
+};
+
+template <bool HOMOG, bool HESS, int NC>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
+    walk4s_kernel(const __grid_constant__ Walk4SParams PS) {
+  using Gm = Walk4SGeom<NC>;
+  constexpr int L = 4, TCC = Gm::TCC, VEC = Gm::VEC, SD2 = Gm::SD2;
+  static_assert(TCC <= SD2, "a TC block fits in an operand slot");
+  const Walk4Params& P4 = PS.w;
+  const WalkParams& p = P4.p;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int warp = blockIdx.x * kWarpsPerBlock + wib;
+  const int TW = gridDim.x * kWarpsPerBlock;
+  const int N = p.N, root = 2 * N - 1;
+  double2* const wsm = reinterpret_cast<double2*>(smem_raw) + size_t(wib) * Gm::WARP;
+  double2* const sQ = wsm;
+  double2* const sA = wsm + SD2;
+  double2* const sB = wsm + 2 * SD2;
+  double2* const sT0 = wsm + 3 * SD2;
+  double2* const sT1 = sT0 + TCC;
+  double2* const sC = sT1 + TCC;  // code rows: [0..1] child 0, [2..3] child 1
+  double2* const sX = sC + 4;     // exponent row of a staged pre-partial
+
+  const size_t wbase = size_t(warp) * size_t(N - 1);
+  const double2* Eb = reinterpret_cast<const double2*>(p.escr + wbase * VEC) + lane - size_t(SD2) * size_t(N + 1);
+  double2* Ew = reinterpret_cast<double2*>(p.escr + wbase * VEC) + lane - size_t(SD2) * size_t(N + 1);
+  double2* Qw = reinterpret_cast<double2*>(p.qscr + wbase * VEC) + lane - size_t(SD2) * size_t(N + 1);
+  int* Xw = PS.qexp + wbase * 32 + lane - size_t(32) * size_t(N + 1);
+  const int* Xb = PS.qexp + wbase * 32 - size_t(32) * size_t(N + 1);
+  double* A = p.acc + size_t(warp) * p.accw;
+  for (int i = lane; i < p.accw; i += 32) A[i] = 0.0;
+  __syncwarp();
+
+  const unsigned long long pol_first = policy_evict_first();
+  auto stage_slot = [&](double2* slot, const double2* gs) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cp16_cg(slot + lane + q * 32, gs + q * 32);
+  };
+  auto stage_slot_once = [&](double2* slot, const double2* gs) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cp16_cg_hint(slot + lane + q * 32, gs + q * 32, pol_first);
+  };
+  auto stage_blk = [&](double2* d, const double* table, int node) {
+    const double2* gs = reinterpret_cast<const double2*>(table) + size_t(node - 1) * TCC;
+#pragma unroll
+    for (int c = 0; c < (TCC + 31) / 32; ++c)
+      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
+  };
+  const size_t Pc = size_t(p.Pc);
+  auto read_cat = [&](const double2* slot, int j, double (&v)[4]) {
+    const double2 a = slot[lane + (2 * j) * 32], b = slot[lane + (2 * j + 1) * 32];
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  };
+  auto write_cat = [&](double2* slot, int j, const double (&v)[4]) {
+    slot[lane + (2 * j) * 32] = make_double2(v[0], v[1]);
+    slot[lane + (2 * j + 1) * 32] = make_double2(v[2], v[3]);
+  };
+  auto gather_cat = [&](const double2* tcs, int code, int j, double (&v)[4]) {
+    const double2* c = tcs + (j * NC + code) * 2;
+    const double2 a = c[0], b = c[1];
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  };
+  auto qm = [&](int x, int r, int c) -> double {
+    if constexpr (HOMOG) return P4.q[r * 4 + c];
+    else return __ldg(p.qtab + size_t(p.qidx[x]) * 16 + r * 4 + c);
+  };
+  auto shfl4 = [&](const int4 v, int src) -> int4 {
+    int4 o;
+    o.x = __shfl_sync(kFull, v.x, src);
+    o.y = __shfl_sync(kFull, v.y, src);
+    o.z = __shfl_sync(kFull, v.z, src);
+    o.w = __shfl_sync(kFull, v.w, src);
+    return o;
+  };
+  // 2^-ex applied by the consumer of a pre-partial (walk4_kernel's emit scale)
+  auto qscale = [](int ex) -> double { return (ex != 0 && ex <= 1022) ? pow2_neg(ex) : 1.0; };
+
+  const int n = p.nsteps;
+  for (int t = warp; t < p.ntiles; t += TW) {
+    const int s = t * 32 + lane;
+    const bool valid = s < p.P;
+    const int sc = valid ? s : p.P - 1;
+    const double w = valid ? p.weights[sc] : 0.0;
+    const uint8_t* codes = p.codes + size_t(t) * 32;  // tile base; row stride Pc
+    auto code_row = [&](double2* d, int tip) {
+      if (lane < 2) cp16_ca(d + lane, codes + size_t(tip - 1) * Pc + 16 * lane);
+    };
+    auto code_at = [&](const double2* d) -> int { return reinterpret_cast<const uint8_t*>(d)[lane]; };
+
+    // ------------------------------------------------ post-order pass (a)
+    {
+      int S = 0;
+      // operands: tip -> TC block 0/1 + code row; the previous step's node ->
+      // slot Q (its edge message, written there in place); else slot A
+      auto issue_ops = [&](const int4 d, int last) {
+        if (d.y <= N) {
+          code_row(sC, d.y);
+          stage_blk(sT0, p.tc, d.y);
+        } else if (d.y != last) {
+          stage_slot(sA, Eb + size_t(d.y) * SD2);
+        }
+        if (d.z <= N) {
+          code_row(sC + 2, d.z);
+          stage_blk(sT1, p.tc, d.z);
+        } else if (d.z != last) {
+          stage_slot(sA, Eb + size_t(d.z) * SD2);
+        }
+      };
+      auto issue_own = [&](const int4 d) {
+        if (d.x != root) stage_blk(sB, p.tc, d.x);
+      };
+      int4 win = lane < n ? p.post[lane] : make_int4(0, 0, 0, 0);
+      int4 winn = 32 + lane < n ? p.post[32 + lane] : make_int4(0, 0, 0, 0);
+      int4 d = shfl4(win, 0);
+      issue_ops(d, -1);
+      issue_own(d);
+      cp_commit();
+      int last = -1;
+      for (int i = 0; i < n; ++i) {
+        int4 dn = make_int4(0, 0, 0, 0);
+        if (i + 1 < n) {
+          const int li = (i + 1) & 31;
+          if (li == 0) {
+            win = winn;
+            winn = i + 33 + lane < n ? p.post[i + 33 + lane] : make_int4(0, 0, 0, 0);
+          }
+          dn = shfl4(win, li);
+        }
+        cpa_wait_all();
+        __syncwarp();
+        const int ka = d.y <= N ? 0 : d.y == last ? 1 : 2;
+        const int kb = d.z <= N ? 0 : d.z == last ? 1 : 2;
+        const int code0 = ka == 0 ? code_at(sC) : 0;
+        const int code1 = kb == 0 ? code_at(sC + 2) : 0;
+        double x[L][4];
+        int hm = 0;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          double a[4], b[4];
+          if (ka == 0) gather_cat(sT0, code0, j, a);
+          else read_cat(ka == 1 ? sQ : sA, j, a);
+          if (kb == 0) gather_cat(sT1, code1, j, b);
+          else read_cat(kb == 1 ? sQ : sA, j, b);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            x[j][r] = a[r] * b[r];
+            hm = max(hm, __double2hiint(x[j][r]));
+          }
+        }
+        __syncwarp();
+        // slot A, the TC blocks and the code rows are free: the next step's operands
+        if (i + 1 < n) issue_ops(dn, d.x);
+        if (!p.disable) {
+          const int ex = peak_exponent(hm);
+          if (ex != 0) {
+            S += ex;
+            if (ex <= 1022) {
+              const double sc2 = pow2_neg(ex);
+#pragma unroll
+              for (int j = 0; j < L; ++j)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) x[j][r] *= sc2;
+            } else {
+#pragma unroll
+              for (int j = 0; j < L; ++j)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) x[j][r] = ldexp(x[j][r], -ex);
+            }
+          }
+        }
+        if (d.x == root) {
+          double mix = 0.0;
+#pragma unroll
+          for (int j = 0; j < L; ++j) {
+            double dd = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) dd = fma(P4.pi[r], x[j][r], dd);
+            mix = fma(PS.cw[j], dd, mix);
+          }
+          const double ll = log(mix) + double(S) * 0.6931471805599453;
+          if (valid) {
+            if (!isfinite(mix)) atomicMin(&p.err[0], s);
+            else if (mix <= 0.0) atomicMin(&p.err[1], s);
+            if (p.site_ll) p.site_ll[s] = ll;
+          }
+          const double v = warp_sum(valid ? w * ll : 0.0);
+          if (lane == 0) atomicAdd(A, v);
+        } else {
+          double2* dst = Ew + size_t(d.x) * SD2;
+#pragma unroll
+          for (int j = 0; j < L; ++j) {
+            const double2* Tl = sB + j * NC * 2;
+            double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double2 a = Tl[2 * c], b = Tl[2 * c + 1];
+              const double xc = x[j][c];
+              e0 = fma(a.x, xc, e0);
+              e1 = fma(a.y, xc, e1);
+              e2 = fma(b.x, xc, e2);
+              e3 = fma(b.y, xc, e3);
+            }
+            // in place: the kept operand of this category was read above
+            sQ[lane + (2 * j) * 32] = make_double2(e0, e1);
+            sQ[lane + (2 * j + 1) * 32] = make_double2(e2, e3);
+            __stcs(dst + (2 * j) * 32, make_double2(e0, e1));
+            __stcs(dst + (2 * j + 1) * 32, make_double2(e2, e3));
+          }
+          last = d.x;
+        }
+        __syncwarp();
+        if (i + 1 < n) issue_own(dn);
+        cp_commit();
+        d = dn;
+      }
+      cpa_wait_all();
+      __syncwarp();
+    }
+    if (!p.do_pre) continue;
+
+    // ----------------------------------- pre-order pass + gradient (b)+(c)
+    {
+      // the step's pre-partial is in slot Q: handed on in place by the
+      // previous step (scale in qs_next) or staged from its scratch slot with
+      // its exponent row; child 0 -> TC 0 + slot A (edge message, or a tip's
+      // Q P table) + code row 0; child 1 -> TC 1, slot B, code row 1
+      auto issue = [&](const int4 d, int handed) {
+        if (d.x != root && handed != d.x) {
+          stage_slot(sQ, Qw + size_t(d.x) * SD2);
+          if (lane < 8) cp16_cg(sX + lane, Xb + size_t(d.x) * 32 + 4 * lane);
+        }
+        if (d.y <= N) {
+          code_row(sC, d.y);
+          stage_blk(sA, p.qtc, d.y);
+        } else {
+          stage_slot_once(sA, Eb + size_t(d.y) * SD2);
+        }
+        if (d.z <= N) {
+          code_row(sC + 2, d.z);
+          stage_blk(sB, p.qtc, d.z);
+        } else {
+          stage_slot_once(sB, Eb + size_t(d.z) * SD2);
+        }
+        stage_blk(sT0, p.tc, d.y);
+        stage_blk(sT1, p.tc, d.z);
+      };
+      const int pf = PS.pf;
+      const char* base_e = reinterpret_cast<const char*>(p.escr + wbase * VEC);
+      int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
+      int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
+      int4 d = shfl4(win, 0);
+      // L2 prefetch of the first steps' edge messages
+      for (int k = 1; k < pf && k < n; ++k) {
+        const int4 f = shfl4(k < 32 ? win : winn, k & 31);
+        if (f.y > N) prefetch_l2(base_e + size_t(f.y - N - 1) * (VEC * 8) + lane * 128);
+        if (f.z > N) prefetch_l2(base_e + size_t(f.z - N - 1) * (VEC * 8) + lane * 128);
+      }
+      issue(d, 0);
+      cp_commit();
+      // the root's pre-partial is pi
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        sQ[lane + (2 * j) * 32] = make_double2(P4.pi[0], P4.pi[1]);
+        sQ[lane + (2 * j + 1) * 32] = make_double2(P4.pi[2], P4.pi[3]);
+      }
+      double qs = 1.0, qs_next = 1.0;
+      int handed = 0;
+      for (int i = 0; i < n; ++i) {
+        int4 dn = make_int4(0, 0, 0, 0);
+        if (i + 1 < n) {
+          const int li = (i + 1) & 31;
+          if (li == 0) {
+            win = winn;
+            winn = i + 33 + lane < n ? p.pre[i + 33 + lane] : make_int4(0, 0, 0, 0);
+          }
+          dn = shfl4(win, li);
+        }
+        if (pf > 0 && i + pf < n) {
+          // win holds the 32 steps from (i + 1) & ~31 (updated above), winn the next 32
+          const int k = i + pf, base = (i + 1) & ~31;
+          const int4 f = shfl4(k - base < 32 ? win : winn, k & 31);
+          if (f.y > N) prefetch_l2(base_e + size_t(f.y - N - 1) * (VEC * 8) + lane * 128);
+          if (f.z > N) prefetch_l2(base_e + size_t(f.z - N - 1) * (VEC * 8) + lane * 128);
+        }
+        cpa_wait_all();
+        __syncwarp();
+        if (d.x == root) qs = 1.0;
+        else if (handed == d.x) qs = qs_next;
+        else qs = qscale(reinterpret_cast<const int*>(sX)[lane]);
+        const bool a_int = d.y > N, b_int = d.z > N;
+        const int code0 = a_int ? 0 : code_at(sC);
+        const int code1 = b_int ? 0 : code_at(sC + 2);
+        // consumed scratch is dead: drop it from L2 without write-back
+        if (lane < VEC / 16) {
+          const char* base_q = reinterpret_cast<const char*>(p.qscr + wbase * VEC);
+          if (a_int) discard_l2(base_e + size_t(d.y - N - 1) * (VEC * 8) + lane * 128);
+          if (b_int) discard_l2(base_e + size_t(d.z - N - 1) * (VEC * 8) + lane * 128);
+          if (d.x != root && handed != d.x) discard_l2(base_q + size_t(d.x - N - 1) * (VEC * 8) + lane * 128);
+        }
+        double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
+        int ha = 0, hb = 0;
+        double2* qa_dst = Qw + size_t(d.y) * SD2;  // lane offset included
+        double2* qb_dst = Qw + size_t(d.z) * SD2;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          double q[4], ea[4], eb[4];
+          read_cat(sQ, j, q);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) q[r] *= qs;
+          if (a_int) read_cat(sA, j, ea);
+          else gather_cat(sT0, code0, j, ea);
+          if (b_int) read_cat(sB, j, eb);
+          else gather_cat(sT1, code1, j, eb);
+          double ta[4], tb[4], dd = 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            ta[r] = q[r] * eb[r];  // top for child a
+            tb[r] = q[r] * ea[r];  // top for child b
+            dd = fma(ta[r], ea[r], dd);
+          }
+          den = fma(PS.cw[j], dd, den);
+          // gradient numerators top . (Q e): a mat-vec for an internal child,
+          // the staged Q P column for a tip (P and Q commute, engine.hpp:260)
+          double qea[4], qeb[4];
+          if (a_int) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              double u = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) u = fma(qm(d.y, r, c), ea[c], u);
+              qea[r] = u;
+            }
+          } else {
+            gather_cat(sA, code0, j, qea);
+          }
+          if (b_int) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              double v = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) v = fma(qm(d.z, r, c), eb[c], v);
+              qeb[r] = v;
+            }
+          } else {
+            gather_cat(sB, code1, j, qeb);
+          }
+          double d1a = 0.0, d1b = 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            d1a = fma(ta[r], qea[r], d1a);
+            d1b = fma(tb[r], qeb[r], d1b);
+          }
+          na = fma(PS.crw[j], d1a, na);
+          nb = fma(PS.crw[j], d1b, nb);
+          if constexpr (HESS) {
+            double d2a = 0.0, d2b = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              double u = 0.0, v = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                u = fma(qm(d.y, r, c), qea[c], u);
+                v = fma(qm(d.z, r, c), qeb[c], v);
+              }
+              d2a = fma(ta[r], u, d2a);
+              d2b = fma(tb[r], v, d2b);
+            }
+            na2 = fma(PS.cr2w[j], d2a, na2);
+            nb2 = fma(PS.cr2w[j], d2b, nb2);
+          }
+          // outgoing pre-partials q_x = P_x^T top (engine.hpp:249-250),
+          // unnormalised: the child visited next in place into slot Q (this
+          // category's q was read above), the other to its scratch slot
+          if (a_int) {
+            const double2* Tl = sT0 + j * NC * 2;
+            double o[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
+              o[c] = fma(u.x, ta[0], fma(u.y, ta[1], fma(v.x, ta[2], v.y * ta[3])));
+              ha = max(ha, __double2hiint(o[c]));
+            }
+            if (d.y == d.w) write_cat(sQ, j, o);
+            else {
+              __stcg(qa_dst + (2 * j) * 32, make_double2(o[0], o[1]));
+              __stcg(qa_dst + (2 * j + 1) * 32, make_double2(o[2], o[3]));
+            }
+          }
+          if (b_int) {
+            const double2* Tl = sT1 + j * NC * 2;
+            double o[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double2 u = Tl[2 * c], v = Tl[2 * c + 1];
+              o[c] = fma(u.x, tb[0], fma(u.y, tb[1], fma(v.x, tb[2], v.y * tb[3])));
+              hb = max(hb, __double2hiint(o[c]));
+            }
+            if (d.z == d.w) write_cat(sQ, j, o);
+            else {
+              __stcg(qb_dst + (2 * j) * 32, make_double2(o[0], o[1]));
+              __stcg(qb_dst + (2 * j + 1) * 32, make_double2(o[2], o[3]));
+            }
+          }
+        }
+        __syncwarp();
+        // the next step's operands (slots A, B, TC blocks, code rows; slot Q
+        // unless its pre-partial was just handed on there)
+        if (i + 1 < n) issue(dn, d.w);
+        cp_commit();
+        const double inv = 1.0 / den;
+        {
+          const double r1a = na * inv, r1b = nb * inv;
+          const double ga = warp_sum(valid ? w * r1a : 0.0);
+          const double gb = warp_sum(valid ? w * r1b : 0.0);
+          if (lane == 0) {
+            atomicAdd(A + d.y, ga);
+            atomicAdd(A + d.z, gb);
+          }
+          if constexpr (HESS) {
+            const double ha2 = warp_sum(valid ? w * (na2 * inv - r1a * r1a) : 0.0);
+            const double hb2 = warp_sum(valid ? w * (nb2 * inv - r1b * r1b) : 0.0);
+            if (lane == 0) {
+              atomicAdd(A + p.B + d.y, ha2);
+              atomicAdd(A + p.B + d.z, hb2);
+            }
+          }
+        }
+        // normalisation exponents of the emitted pre-partials
+        if (a_int) {
+          const int ex = peak_exponent(ha);
+          if (d.y == d.w) qs_next = qscale(ex);
+          else Xw[size_t(d.y) * 32] = ex;
+        }
+        if (b_int) {
+          const int ex = peak_exponent(hb);
+          if (d.z == d.w) qs_next = qscale(ex);
+          else Xw[size_t(d.z) * 32] = ex;
+        }
+        handed = d.w;
+        d = dn;
+      }
+      cpa_wait_all();
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace pgk

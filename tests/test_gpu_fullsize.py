@@ -32,7 +32,7 @@ def _fixture(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,kernel,lanes", [("C2", "walk4_kernel", 2), ("C3", "walk4_kernel", 1),
+@pytest.mark.parametrize("name,kernel,lanes", [("C2", "walk4_kernel", 2), ("C3", "walk4s_kernel", 1),
                                                ("C4", "walkm_kernel", 4), ("C5", "walkm_kernel", 4)])
 def test_full_size_workload_matches_oracle(name, kernel, lanes):
     fx = _fixture(name)
