@@ -637,10 +637,8 @@ struct pg_engine {
       use_walk4s = lane1 && pg_walk4s_kernel(true, false, NC) != nullptr;
       if (const char* v = std::getenv("PG_WALK4S")) use_walk4s = use_walk4s && std::atoi(v) != 0;
       if (const char* v = std::getenv("PG_WALK4S_PF")) walk4s_pf = std::max(0, std::min(31, std::atoi(v)));
-      const size_t tcb = size_t(L) * NC * 4;
       walk_smem = use_walk4s ? pg_walk4s_smem(NC)
-                             : size_t(pgk::kWarpsPerBlock) * 2 * (3 * (32 * walk4_lcv * 4 / 2) + 3 * (tcb / 2) + 4) *
-                                   sizeof(double2);
+                             : size_t(pgk::kWarpsPerBlock) * 2 * pgk::walk4_stage_d2(walk4_lcv, L, NC) * sizeof(double2);
     }
     if (use_walkl) {
       G = L;

@@ -66,6 +66,14 @@ __device__ __forceinline__ int peak_exponent(int hmax) {
 // 2^-ex as a double (exact; ex in [-1021, 1022]).
 __device__ __forceinline__ double pow2_neg(int ex) { return __hiloint2double((1023 - ex) << 20, 0); }
 
+// double2 per shared-memory stage of one warp: 3 operand slots, 3 TC blocks,
+// 2 x 32 B code rows, rounded up to 128 bytes so every warp-wide 512-byte slot
+// access is 4 wavefronts (an odd 64-byte offset made it 5: 23 % excessive
+// shared wavefronts in the C3 capture, profiles/r23_walk4_C3_100k_smem.txt)
+__host__ __device__ constexpr int walk4_stage_d2(int LCV, int LT, int NC) {
+  return (3 * (32 * LCV * 4 / 2) + 3 * (LT * NC * 4 / 2) + 4 + 7) & ~7;
+}
+
 // LT = rate categories (4, 2 or 1); LCV = categories per lane (LT: one lane
 // per pattern, 32 patterns per warp tile; LT/2: two lanes per pattern, 16
 // patterns per tile, half the registers and shared memory per warp -> more
@@ -82,7 +90,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   constexpr int TCC = TCB / 2;               // double2 chunks per TC block
   constexpr int VEC = 32 * LCV * MP;         // doubles per node slot of one warp
   constexpr int SD2 = VEC / 2;               // double2 per node slot
-  constexpr int STAGE = 3 * SD2 + 3 * TCC + 4;  // double2 per stage: 3 operand slots, 3 TC blocks, 2x32 B codes
+  constexpr int STAGE = walk4_stage_d2(LCV, LT, NC);  // double2 per stage (128-byte aligned)
+  static_assert(STAGE >= 3 * SD2 + 3 * TCC + 4, "stage holds 3 slots, 3 TC blocks and the code rows");
   static_assert(TCC <= SD2, "a TC block fits in an operand slot");
   const WalkParams& p = P4.p;
   extern __shared__ __align__(16) unsigned char smem_raw[];

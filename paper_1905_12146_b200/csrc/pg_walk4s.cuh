@@ -12,7 +12,7 @@
 //  * one shared-memory stage per warp: slots Q (the step's pre-partial, or
 //    the post-order edge message handed to the next step), A and B (the
 //    children's staged edge messages, or a tip child's Q P table), two TC
-//    blocks and the tip code rows (13.8 KB per warp);
+//    blocks and the tip code rows (13.8 KB per warp, 128-byte aligned);
 //  * results are written in place: a post-order step's edge message goes to
 //    slot Q category by category after that category's operands are read, a
 //    pre-order step's outgoing pre-partial for the child visited next
@@ -51,7 +51,8 @@ struct Walk4SGeom {
   static constexpr int VEC = 32 * L * MP;  // doubles per node slot of one warp
   static constexpr int SD2 = VEC / 2;      // double2 per node slot
   // per warp: slots Q, A, B; TC blocks 0, 1; code rows (2 x 32 B); exponent row (32 ints)
-  static constexpr int WARP = 3 * SD2 + 2 * TCC + 4 + 8;  // double2
+  // (rounded up to 128 bytes: a 64-byte offset makes every 512-byte slot access 5 wavefronts)
+  static constexpr int WARP = (3 * SD2 + 2 * TCC + 4 + 8 + 7) & ~7;  // double2
 };
 
 template <bool HOMOG, bool HESS, int NC>
