@@ -177,7 +177,8 @@ int pg_engine_info(const pg_engine* e, int* launches, int* total_warps, int* lan
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms);
 /* Walk-kernel variant of the current geometry: 0 generic register-tiled
  * walk_kernel<MP,LC>, 1 pipelined 4-state walk4_kernel, 2 DMMA large-state walkm_kernel,
- * 3 level-scheduled walkl_kernel, 4 single-buffered 4-state walk4s_kernel. */
+ * 3 level-scheduled walkl_kernel, 4 single-buffered 4-state walk4s_kernel, 5 tensor-core 4-state
+ * walk4t_kernel. */
 int pg_engine_variant(const pg_engine* e);
 /* Per-evaluation CUDA-event timing on the engine stream: returns the number of
  * evaluations recorded since the previous call and the summed device ms of the

@@ -683,7 +683,7 @@ class LikelihoodEngine:
         check(lib().pg_engine_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
         return {"launches": a.value, "total_warps": b.value, "lanes_per_pattern": c.value, "padded_states": d.value,
                 "kernel": ["walk_kernel", "walk4_kernel", "walkm_kernel",
-                           "walkl_kernel", "walk4s_kernel"][lib().pg_engine_variant(self._h)]}
+                           "walkl_kernel", "walk4s_kernel", "walk4t_kernel"][lib().pg_engine_variant(self._h)]}
 
     def last_times_ms(self):
         w, t = C.c_float(), C.c_float()

@@ -28,6 +28,8 @@ void* pg_walk4_kernel_lc2(bool homog, bool hess, int nc);
 void* pg_walk4_kernel_l12(bool homog, bool hess, int nc, int L);
 // L = 4: lcv 4 (one lane per pattern) or 2 (two lanes); L = 1, 2: one lane
 void* pg_walk4s_kernel(bool homog, bool hess, int nc);
+void* pg_walk4t_kernel(bool hess, int nc);
+size_t pg_walk4t_smem(int nc);
 size_t pg_walk4s_smem(int nc);
 static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
   if (L != 4) return pg_walk4_kernel_l12(homog, hess, nc, L);
@@ -147,6 +149,7 @@ struct pg_engine {
   int codes_mp = 0;        // MP the device tip codes' class columns are encoded for
   int walkm_wpc = 4;       // warps per CTA in walkm
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
+  bool use_walk4t = false;  // tensor-core (DMMA) variant (L = 4, one lane per pattern state)
   bool use_walk4s = false;  // single-buffered variant (L = 4, one lane per pattern): 16 warps per SM
   int walk4s_pf = 0;        // its L2 prefetch distance (steps; measured neutral on C3: 0/2/3 145.2/146.8/147.7 ms)
   size_t walk_smem = 0;
@@ -154,7 +157,7 @@ struct pg_engine {
 
   // device state
   DevBuf<uint8_t> d_codes;
-  DevBuf<double> d_qtc, d_fpp, d_fpt, d_fq;
+  DevBuf<double> d_qtc, d_fpp, d_fpt, d_fq, d_f4post, d_f4pre;
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err, d_qexp;
   DevBuf<int4> d_post, d_pre;
@@ -637,7 +640,11 @@ struct pg_engine {
       use_walk4s = lane1 && pg_walk4s_kernel(true, false, NC) != nullptr;
       if (const char* v = std::getenv("PG_WALK4S")) use_walk4s = use_walk4s && std::atoi(v) != 0;
       if (const char* v = std::getenv("PG_WALK4S_PF")) walk4s_pf = std::max(0, std::min(31, std::atoi(v)));
-      walk_smem = use_walk4s ? pg_walk4s_smem(NC)
+      use_walk4t = lane1 && pg_walk4t_kernel(false, NC) != nullptr && std::getenv("PG_WALK4T") != nullptr &&
+                   std::atoi(std::getenv("PG_WALK4T")) != 0;
+      if (use_walk4t) use_walk4s = false;
+      walk_smem = use_walk4t   ? pg_walk4t_smem(NC)
+                  : use_walk4s ? pg_walk4s_smem(NC)
                              : size_t(pgk::kWarpsPerBlock) * 2 * pgk::walk4_stage_d2(walk4_lcv, L, NC) * sizeof(double2);
     }
     if (use_walkl) {
@@ -700,6 +707,10 @@ struct pg_engine {
       d_qscr.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * vec);
     }
     if (use_walk4 && use_walk4s) d_qexp.ensure(size_t(TW) * size_t(std::max(N - 1, 1)) * 32);
+    if (use_walk4 && use_walk4t) {
+      d_f4post.ensure(size_t(B()) * L * 32);
+      d_f4pre.ensure(size_t(B()) * (L + 1) * 32);
+    }
     d_acc.ensure(size_t(TW) * size_t(accw));
     d_out.ensure(size_t(accw));
     d_site_ll.ensure(size_t(std::max(P, 1)));
@@ -945,8 +956,9 @@ int pg_engine::walk_max_blocks_per_sm() {
   if (use_walk4) {
     // occupancy of the model's variants (with and without the Hessian) bounds the grid
     for (int v = 0; v < 2; ++v) {
-      const void* fn = use_walk4s ? pg_walk4s_kernel(branch_q.empty(), v & 1, NC)
-                                  : pg_walk4_kernel(branch_q.empty(), v & 1, NC, walk4_lcv, L);
+      const void* fn = use_walk4t   ? pg_walk4t_kernel(v & 1, NC)
+                       : use_walk4s ? pg_walk4s_kernel(branch_q.empty(), v & 1, NC)
+                                    : pg_walk4_kernel(branch_q.empty(), v & 1, NC, walk4_lcv, L);
       PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
@@ -972,6 +984,8 @@ void pg_engine::launch_tc() {
   p.qtc = (use_walkm || use_walk4 || use_walkl) ? d_qtc.p : nullptr;
   p.fpp = use_walkm ? d_fpp.p : nullptr;
   p.fpt = use_walkm ? d_fpt.p : nullptr;
+  p.f4post = (use_walk4 && use_walk4t) ? d_f4post.p : nullptr;
+  p.f4pre = (use_walk4 && use_walk4t) ? d_f4pre.p : nullptr;
   p.err = d_err.p;
   p.m = m;
   p.MP = MP;
@@ -1069,7 +1083,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       p4.pi[i] = i < m ? pi[size_t(i)] : 0.0;
       for (int j = 0; j < 4; ++j) p4.q[i * 4 + j] = (i < m && j < m) ? q[size_t(i) * m + j] : 0.0;
     }
-    if (use_walk4s) {
+    if (use_walk4s || use_walk4t) {
       pgk::Walk4SParams ps{};
       ps.w = p4;
       for (int l = 0; l < 4; ++l) {
@@ -1080,6 +1094,17 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       }
       ps.qexp = d_qexp.p;
       ps.pf = walk4s_pf;
+      if (use_walk4t) {
+        pgk::Walk4TParams pt{};
+        pt.s = ps;
+        pt.f4post = d_f4post.p;
+        pt.f4pre = d_f4pre.p;
+        void* fn = pg_walk4t_kernel(do_hess, NC);
+        void* args[] = {&pt};
+        PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
+                                 walk_smem, stream));
+        return;
+      }
       void* fn = pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
       void* args[] = {&ps};
       PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
@@ -1601,7 +1626,7 @@ int pg_timing(pg_engine* e, int enable, int* evaluations, double* walk_ms_total,
 
 int pg_engine_variant(const pg_engine* e) {
   e = primary(e);
-  return e->use_walkm ? 2 : e->use_walkl ? 3 : e->use_walk4 ? (e->use_walk4s ? 4 : 1) : 0;
+  return e->use_walkm ? 2 : e->use_walkl ? 3 : e->use_walk4 ? (e->use_walk4t ? 5 : e->use_walk4s ? 4 : 1) : 0;
 }
 
 int pg_last_walk_ms(const pg_engine* e, float* walk_ms, float* total_ms) {

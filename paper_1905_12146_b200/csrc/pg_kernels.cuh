@@ -113,6 +113,9 @@ struct TcParams {
   double* qtc;          // optional [B][L][NC][MP]: the same columns of Q_branch * P (tip Q-e gathers)
   double* fpp;          // optional [B][L][MP*MP]: P in DMMA B-fragment order for y = P x (walkm)
   double* fpt;          // optional [B][L][MP*MP]: same for y = P^T x
+  double* f4post;       // optional [B][L][32]: 4-state P in m8n8k4 B-fragment order for e = P x (walk4t)
+  double* f4pre;        // optional [B][L+1][32]: [l] P^T x in the even, Q^T x in the odd output columns;
+                        //   [L] (Q^2)^T x in the even columns (walk4t)
   int* err;             // err[2] <- 1 on a negative / non-finite branch length
   int m, MP, NC, A, L, have_eigen;
 };
@@ -324,6 +327,31 @@ __global__ void tc_kernel(const __grid_constant__ TcParams p) {
       const int at = frag_pos(f, lane, KK * NT);
       fp[at] = in ? R[n * m + k] : 0.0;  // y = P x: M(k, n) = P[n][k]
       ft[at] = in ? R[k * m + n] : 0.0;  // y = P^T x: M(k, n) = P[k][n]
+    }
+  }
+  if (p.f4post && m <= 4) {
+    // m8n8k4 B fragments for walk4t (lane t holds B[kk = t%4][n = t/4]); the
+    // vector layout there is lane = (pattern, state kk), so output column
+    // n = 2c lands on the lane of state c: even columns carry the result in
+    // that layout, odd columns a second product of the same A
+    const double* Q = p.qtab + size_t(qi) * p.MP * p.MP;
+    double* fo = p.f4post + (size_t(node - 1) * p.L + l) * 32;
+    double* fr = p.f4pre + (size_t(node - 1) * (p.L + 1) + l) * 32;
+    for (int e = threadIdx.x; e < 32; e += blockDim.x) {
+      const int kk = e & 3, n = e >> 2, c = n >> 1;
+      const bool in = kk < m && c < m, odd = n & 1;
+      fo[e] = (in && !odd) ? R[c * m + kk] : 0.0;                     // e[c] = sum_kk P[c][kk] x[kk]
+      fr[e] = !in ? 0.0 : odd ? Q[kk * p.MP + c] : R[kk * m + c];     // q[c] = (P^T t)[c], u[c] = (Q^T t)[c]
+    }
+    if (l == 0) {
+      double* fh = p.f4pre + (size_t(node - 1) * (p.L + 1) + p.L) * 32;
+      for (int e = threadIdx.x; e < 32; e += blockDim.x) {
+        const int kk = e & 3, n = e >> 2, c = n >> 1;
+        double v = 0.0;
+        if (kk < m && c < m && !(n & 1))
+          for (int j = 0; j < m; ++j) v = fma(Q[kk * p.MP + j], Q[j * p.MP + c], v);  // (Q^2)[kk][c]
+        fh[e] = v;
+      }
     }
   }
   if (p.qtc) {

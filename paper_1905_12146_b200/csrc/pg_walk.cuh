@@ -127,6 +127,13 @@ struct Walk4SParams {
   int pf;                          // L2 prefetch distance (steps) of the edge messages the pre pass reads
 };
 
+// Parameters of the tensor-core 4-state kernel (pg_walk4t.cuh).
+struct Walk4TParams {
+  Walk4SParams s;
+  const double* f4post;  // [B][L][32] B fragments of e = P x
+  const double* f4pre;   // [B][L+1][32] B fragments of (P^T t | Q^T t), [L]: (Q^2)^T t
+};
+
 // Parameters of the DMMA large-state kernel (pg_walkm.cuh).
 struct WalkMParams {
   WalkParams p;

@@ -18,13 +18,19 @@ from paper_1905_12146_b200.api import (EngineOptions, LikelihoodEngine, RateCate
                                        SitePatternAlignment, SubstitutionModel, Tree, parse_fasta, parse_newick)
 
 
-@pytest.fixture(params=["lvl", "4s", 4, 2], ids=["walkl", "lcv4s", "lcv4", "lcv2"])
+@pytest.fixture(params=["lvl", "4t", "4s", 4, 2], ids=["walkl", "lcv4t", "lcv4s", "lcv4", "lcv2"])
 def lcv(request, monkeypatch):
     """The kernel variant under test; returns (kernel name, lanes per pattern)."""
     if request.param == "lvl":
         monkeypatch.setenv("PG_WALKL", "1")
         return "walkl_kernel", 4
     monkeypatch.setenv("PG_WALKL", "0")
+    if request.param == "4t":
+        # tensor-core (DMMA) walk: lane = (pattern, state)
+        monkeypatch.setenv("PG_WALK4_LCV", "4")
+        monkeypatch.setenv("PG_WALK4T", "1")
+        return "walk4t_kernel", 1
+    monkeypatch.setenv("PG_WALK4T", "0")
     if request.param == "4s":
         # single-buffered one-lane-per-pattern walk (the default at large P)
         monkeypatch.setenv("PG_WALK4_LCV", "4")
