@@ -9,7 +9,7 @@ for v in ${VARIANTS}; do
   for c in ${CONFIGS:-C3}; do
     env ${envs//,/ } timeout 900 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/ab_${name}_$c.json 2>gpurun_out/ab_${name}_$c.err
     python -c "
-import json; d=json.load(open('gpurun_out/ab_${name}_$c.json')); r=d['roofline']; p=d.get('parity',{})
+import json; d=json.load(open('gpurun_out/ab_${name}_$c.json')); r=d['roofline']; p=d.get('parity') or {}
 print('$name $c', round(d['ms_per_step'],2), 'ms walk', round(r['walk_ms'],2), 'frac', round(r['frac'],3), d['geometry']['kernel'], 'parity', p.get('within_1e-9'), p.get('grad_max_rel_to_condition'))" 2>&1 | tail -1
   done
 done

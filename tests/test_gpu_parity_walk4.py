@@ -32,8 +32,10 @@ def lcv(request, monkeypatch):
         return "walk4t_kernel", 1
     monkeypatch.setenv("PG_WALK4T", "0")
     if request.param == "4s":
-        # single-buffered one-lane-per-pattern walk (the default at large P)
+        # single-buffered one-lane-per-pattern walk (chosen by padded wave
+        # work at large P; forced here)
         monkeypatch.setenv("PG_WALK4_LCV", "4")
+        monkeypatch.setenv("PG_WALK4S", "1")
         return "walk4s_kernel", 1
     monkeypatch.setenv("PG_WALK4S", "0")
     monkeypatch.setenv("PG_WALK4_LCV", str(request.param))
