@@ -561,6 +561,7 @@ struct pg_engine {
   }
 
   int walk_max_blocks_per_sm();
+  int walk_max_blocks_per_sm_occ();
 
   void prepare_geometry() {
     // DMMA kernel for every state space above 4 (m = 5..8 on walkm<8>: 1.8x
@@ -936,6 +937,12 @@ void* select_walk(int MP, int LC) {
 }  // namespace
 
 int pg_engine::walk_max_blocks_per_sm() {
+  // PG_WALK_MAXB caps the resident CTAs per SM (occupancy experiments)
+  const int cap = std::getenv("PG_WALK_MAXB") ? std::max(1, std::atoi(std::getenv("PG_WALK_MAXB"))) : INT_MAX;
+  return std::min(cap, walk_max_blocks_per_sm_occ());
+}
+
+int pg_engine::walk_max_blocks_per_sm_occ() {
   int nb = 0;
   if (use_walkm) {
     for (int h = 0; h < 2; ++h) {

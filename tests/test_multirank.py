@@ -241,3 +241,66 @@ def test_bench_relaunches_under_torchrun(monkeypatch):
     monkeypatch.setenv("WORLD_SIZE", "2")
     assert bench.relaunch_command(args, []) is None
     assert bench.main(["--gpus", "4"]) == 2
+
+
+def _product_worker(rank, world, port, q):
+    """One rank of the sharded product on the GPU: the CUDA LikelihoodEngine
+    over this rank's pattern block, the [logL, g, H] all-reduce over gloo
+    (host tensors -- no rank's kernel waits on another's)."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_1905_12146_b200.sharding import ShardedEngine
+        from workloads import synth
+
+        inst = synth.generate("C3", seed=13, sites=20000, tips=128)
+        sh = ShardedEngine(*synth.api_objects(inst))
+        assert not sh._device_path and hasattr(sh.local, "handle")  # the CUDA engine, host reduction
+        sh.set_clock_durations(inst.durations)
+        rep = sh.branch_gradient(True)
+        rrep = sh.rate_gradient()
+        q.put((rank, rep.log_likelihood, rep.branch_gradient, rep.hessian_diagonal, rrep.branch_gradient,
+               sh.p1 - sh.p0, sh.local.info()["kernel"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_product_on_gpu(world):
+    """The multi-GPU path with the product as the local engine: `world`
+    processes each evaluate their contiguous pattern block with the CUDA
+    engine; the reduced logL, gradient, Hessian and rate gradient equal the
+    unsharded product evaluation (summation order only) and the oracle."""
+    from tests.helpers import assert_logl, assert_vec, oracle_for
+    from workloads import synth
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_product_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+
+    inst = synth.generate("C3", seed=13, sites=20000, tips=128)
+    assert sum(r[5] for r in results) == inst.patterns
+    eng = synth.engine_for(inst)
+    whole = eng.branch_gradient(True)
+    ll, g, h = oracle_for(inst, blocks=8).branch_gradient(True)
+    for _, rll, rg, rh, rr, _, kernel in results:
+        # every rank holds the same reduced result
+        assert rll == results[0][1] and np.array_equal(rg, results[0][2])
+        assert rll == pytest.approx(whole.log_likelihood, rel=1e-13)
+        np.testing.assert_allclose(rg, whole.branch_gradient, rtol=1e-11,
+                                   atol=1e-13 * np.abs(whole.branch_gradient).max())
+        assert_logl(rll, ll)
+        assert_vec(rg, g)
+        assert_vec(rh, h, rtol=1e-8, what="hessian")
+        assert_vec(rr, inst.durations * g, what="rate gradient")
