@@ -148,6 +148,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
+// sums of a over the warp in lane 0 and of b in lane 16 (one butterfly for
+// two values: the first level exchanges halves)
+__device__ __forceinline__ double warp_sum2(double a, double b) {
+  const bool lo = (threadIdx.x & 16) == 0;
+  double v = (lo ? a : b) + __shfl_xor_sync(kFull, lo ? b : a, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
 __device__ __forceinline__ double group_sum(double v, int G) {
   for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;

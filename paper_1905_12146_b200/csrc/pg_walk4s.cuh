@@ -145,10 +145,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     const int sc = valid ? s : p.P - 1;
     const double w = valid ? p.weights[sc] : 0.0;
     const uint8_t* codes = p.codes + size_t(t) * 32;  // tile base; row stride Pc
-    auto code_row = [&](double2* d, int tip) {
-      if (lane < 2) cp16_ca(d + lane, codes + size_t(tip - 1) * Pc + 16 * lane);
-    };
-    auto code_at = [&](const double2* d) -> int { return reinterpret_cast<const uint8_t*>(d)[lane]; };
+    // a tip's code for the lane's pattern, loaded into a register when the
+    // step is issued (consumed one step later; cheaper than staging the
+    // 32-byte row through shared memory: C3 18 instructions per step)
+    auto code_ld = [&](int tip) -> int { return __ldg(codes + size_t(tip - 1) * Pc + lane); };
+    int cn0 = 0, cn1 = 0;  // the next step's tip codes
 
     // ------------------------------------------------ post-order pass (a)
     {
@@ -157,13 +158,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       // slot Q (its edge message, written there in place); else slot A
       auto issue_ops = [&](const int4 d, int last) {
         if (d.y <= N) {
-          code_row(sC, d.y);
+          cn0 = code_ld(d.y);
           stage_blk(sT0, p.tc, d.y);
         } else if (d.y != last) {
           stage_slot(sA, Eb + size_t(d.y) * SD2);
         }
         if (d.z <= N) {
-          code_row(sC + 2, d.z);
+          cn1 = code_ld(d.z);
           stage_blk(sT1, p.tc, d.z);
         } else if (d.z != last) {
           stage_slot(sA, Eb + size_t(d.z) * SD2);
@@ -193,8 +194,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         __syncwarp();
         const int ka = d.y <= N ? 0 : d.y == last ? 1 : 2;
         const int kb = d.z <= N ? 0 : d.z == last ? 1 : 2;
-        const int code0 = ka == 0 ? code_at(sC) : 0;
-        const int code1 = kb == 0 ? code_at(sC + 2) : 0;
+        const int code0 = cn0, code1 = cn1;
         double x[L][4];
         int hm = 0;
 #pragma unroll
@@ -293,13 +293,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           if (lane < 8) cp16_cg(sX + lane, Xb + size_t(d.x) * 32 + 4 * lane);
         }
         if (d.y <= N) {
-          code_row(sC, d.y);
+          cn0 = code_ld(d.y);
           stage_blk(sA, p.qtc, d.y);
         } else {
           stage_slot_once(sA, Eb + size_t(d.y) * SD2);
         }
         if (d.z <= N) {
-          code_row(sC + 2, d.z);
+          cn1 = code_ld(d.z);
           stage_blk(sB, p.qtc, d.z);
         } else {
           stage_slot_once(sB, Eb + size_t(d.z) * SD2);
@@ -351,8 +351,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         else if (handed == d.x) qs = qs_next;
         else qs = qscale(reinterpret_cast<const int*>(sX)[lane]);
         const bool a_int = d.y > N, b_int = d.z > N;
-        const int code0 = a_int ? 0 : code_at(sC);
-        const int code1 = b_int ? 0 : code_at(sC + 2);
+        const int code0 = cn0, code1 = cn1;
         // consumed scratch is dead: drop it from L2 without write-back
         if (lane < VEC / 16) {
           const char* base_q = reinterpret_cast<const char*>(p.qscr + wbase * VEC);
@@ -473,19 +472,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         const double inv = 1.0 / den;
         {
           const double r1a = na * inv, r1b = nb * inv;
-          const double ga = warp_sum(valid ? w * r1a : 0.0);
-          const double gb = warp_sum(valid ? w * r1b : 0.0);
-          if (lane == 0) {
-            atomicAdd(A + d.y, ga);
-            atomicAdd(A + d.z, gb);
-          }
+          // both children's sums in one butterfly: lane 0 gets child a's, lane 16 child b's
+          const double g2 = warp_sum2(valid ? w * r1a : 0.0, valid ? w * r1b : 0.0);
+          if ((lane & 15) == 0) atomicAdd(A + (lane == 0 ? d.y : d.z), g2);
           if constexpr (HESS) {
-            const double ha2 = warp_sum(valid ? w * (na2 * inv - r1a * r1a) : 0.0);
-            const double hb2 = warp_sum(valid ? w * (nb2 * inv - r1b * r1b) : 0.0);
-            if (lane == 0) {
-              atomicAdd(A + p.B + d.y, ha2);
-              atomicAdd(A + p.B + d.z, hb2);
-            }
+            const double h2 = warp_sum2(valid ? w * (na2 * inv - r1a * r1a) : 0.0,
+                                        valid ? w * (nb2 * inv - r1b * r1b) : 0.0);
+            if ((lane & 15) == 0) atomicAdd(A + p.B + (lane == 0 ? d.y : d.z), h2);
           }
         }
         // normalisation exponents of the emitted pre-partials
