@@ -115,6 +115,7 @@ struct pg_engine {
   std::vector<int4> post_steps, pre_steps;
   // patterns
   int m_aln = 0, P = 0, A = 0;
+  bool classes_used = true;  // some tip code is missing (-1) or an ambiguity class
   int64_t Pc = 0;  // device row stride of the tip codes
   bool has_patterns = false;
   std::vector<double> amb;  // [A][m]
@@ -346,10 +347,12 @@ struct pg_engine {
     // warp tile's codes of one tip are 32 aligned bytes (cp.async staging)
     const int64_t pc = (int64_t(np) + 31) / 32 * 32;
     std::vector<uint8_t> col(size_t(N) * size_t(std::max<int64_t>(pc, 32)), 0);
+    bool cls = false;
     for (int t = 0; t < N; ++t)
       for (int s = 0; s < np; ++s) {
         const int c = codes[size_t(t) * size_t(np) + size_t(s)];
         if (c < -1 || c >= mm + na) throw std::invalid_argument("alignment: state code out of range");
+        cls = cls || c < 0 || c >= mm;
         col[size_t(t) * size_t(pc) + size_t(s)] = uint8_t(c < 0 ? mp + na : c < mm ? c : mp + (c - mm));
       }
     std::vector<double> ambv(size_t(na + 1) * mm, 1.0);
@@ -370,6 +373,7 @@ struct pg_engine {
     P = np;
     Pc = int64_t(std::max<int64_t>(pc, 32));
     A = na + 1;
+    classes_used = cls;
     amb = ambv;
     has_patterns = true;
     geometry_dirty = tc_dirty = true;
@@ -646,6 +650,9 @@ struct pg_engine {
       use_walk4t = lane1 && pg_walk4t_kernel(false, NC) != nullptr && std::getenv("PG_WALK4T") != nullptr &&
                    std::atoi(std::getenv("PG_WALK4T")) != 0;
       if (use_walk4t) use_walk4s = false;
+      // no missing / ambiguous tip codes (C3): TC blocks of the 4 state
+      // columns only, one 16-byte chunk per lane (PG_WALK4S_NC5=1 keeps 5)
+      if (use_walk4s && !classes_used && m == 4 && std::getenv("PG_WALK4S_NC5") == nullptr) NC = 4;
       walk_smem = use_walk4t   ? pg_walk4t_smem(NC)
                   : use_walk4s ? pg_walk4s_smem(NC)
                              : size_t(pgk::kWarpsPerBlock) * 2 * pgk::walk4_stage_d2(walk4_lcv, L, NC) * sizeof(double2);

@@ -1,12 +1,17 @@
 // Instantiations of the single-buffered 4-state walk (pg_walk4s.cuh): 4 rate
 // categories, one lane per pattern, homogeneous / per-branch generators x
-// with / without the Hessian x TC column counts NC in {5, 16}.
+// with / without the Hessian x TC column counts NC in {4 (no missing /
+// ambiguous codes), 5, 16}.
 #include "pg_walk4s.cuh"
 
 #define PG_W4S(H, S, NC) \
   if (homog == H && hess == S && nc == NC) return reinterpret_cast<void*>(&pgk::walk4s_kernel<H, S, NC>);
 
 void* pg_walk4s_kernel(bool homog, bool hess, int nc) {
+  PG_W4S(true, false, 4)
+  PG_W4S(true, true, 4)
+  PG_W4S(false, false, 4)
+  PG_W4S(false, true, 4)
   PG_W4S(true, false, 5)
   PG_W4S(true, true, 5)
   PG_W4S(false, false, 5)
@@ -19,6 +24,8 @@ void* pg_walk4s_kernel(bool homog, bool hess, int nc) {
 }
 
 size_t pg_walk4s_smem(int nc) {
-  const size_t warp = nc <= 5 ? pgk::Walk4SGeom<5>::WARP : pgk::Walk4SGeom<16>::WARP;
+  const size_t warp = nc <= 4   ? pgk::Walk4SGeom<4>::WARP
+                      : nc <= 5 ? pgk::Walk4SGeom<5>::WARP
+                                : pgk::Walk4SGeom<16>::WARP;
   return size_t(pgk::kWarpsPerBlock) * warp * sizeof(double2);
 }
