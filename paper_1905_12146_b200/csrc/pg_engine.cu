@@ -152,7 +152,6 @@ struct pg_engine {
   int walk4_lcv = 4;  // categories per lane of the 4-state kernel
   bool use_walk4t = false;  // tensor-core (DMMA) variant (L = 4, one lane per pattern state)
   bool use_walk4s = false;  // single-buffered variant (L = 4, one lane per pattern): 16 warps per SM
-  int walk4s_pf = 0;        // its L2 prefetch distance (steps; measured neutral on C3: 0/2/3 145.2/146.8/147.7 ms)
   size_t walk_smem = 0;
   bool geometry_dirty = true, model_dirty = true, tc_dirty = true, patterns_dirty = true;
 
@@ -646,7 +645,6 @@ struct pg_engine {
       // (measured also on C3 slices, the shard sizes of 2-8 GPUs: 116,972
       // patterns 19.4 vs 22.8 ms, 458,456 patterns 72.0 vs 76.2 ms)
       if (const char* v = std::getenv("PG_WALK4S")) use_walk4s = lane1 && std::atoi(v) != 0;
-      if (const char* v = std::getenv("PG_WALK4S_PF")) walk4s_pf = std::max(0, std::min(31, std::atoi(v)));
       use_walk4t = lane1 && pg_walk4t_kernel(false, NC) != nullptr && std::getenv("PG_WALK4T") != nullptr &&
                    std::atoi(std::getenv("PG_WALK4T")) != 0;
       if (use_walk4t) use_walk4s = false;
@@ -1109,7 +1107,6 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
         ps.cr2w[l] = r * r * w;
       }
       ps.qexp = d_qexp.p;
-      ps.pf = walk4s_pf;
       if (use_walk4t) {
         pgk::Walk4TParams pt{};
         pt.s = ps;

@@ -124,7 +124,6 @@ struct Walk4SParams {
   Walk4Params w;
   double cw[4], crw[4], cr2w[4];  // category weights w_l, c_l w_l, c_l^2 w_l (constant-bank operands)
   int* qexp;                       // [TW][N-1][32] normalisation exponents of the deferred pre-partials
-  int pf;                          // L2 prefetch distance (steps) of the edge messages the pre pass reads
 };
 
 // Parameters of the tensor-core 4-state kernel (pg_walk4t.cuh).

@@ -25,8 +25,11 @@
 //    values as walk4_kernel's, multiplied at read instead of at write;
 //  * a step's loads are issued once the previous step has consumed its
 //    operands and waited on at the top of the step; latency is hidden by the
-//    other warps (up to 16 per SM), and the edge messages the pre-order pass
-//    reads from DRAM are prefetched into L2 `pf` steps ahead.
+//    other warps (up to 16 per SM).  Measured neutral and removed: an L2
+//    prefetch of the edge messages the pre-order pass reads, 2 or 3 steps
+//    ahead (C3 145.2 / 146.8 / 147.7 ms at distance 0 / 2 / 3), and the step
+//    list in the kernel parameters (constant bank) instead of the shuffled
+//    register window (133.0 / 133.4 vs 133.7 / 132.8 ms).
 // Arithmetic and operation order per value are walk4_kernel's, so results are
 // bit-identical to it.
 #pragma once
@@ -38,10 +41,6 @@
 #endif
 
 namespace pgk {
-
-__device__ __forceinline__ void prefetch_l2(const void* gmem) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
-}
 
 template <int NC>
 struct Walk4SGeom {
@@ -307,17 +306,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         stage_blk(sT0, p.tc, d.y);
         stage_blk(sT1, p.tc, d.z);
       };
-      const int pf = PS.pf;
       const char* base_e = reinterpret_cast<const char*>(p.escr + wbase * VEC);
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
       int4 d = shfl4(win, 0);
-      // L2 prefetch of the first steps' edge messages
-      for (int k = 1; k < pf && k < n; ++k) {
-        const int4 f = shfl4(k < 32 ? win : winn, k & 31);
-        if (f.y > N) prefetch_l2(base_e + size_t(f.y - N - 1) * (VEC * 8) + lane * 128);
-        if (f.z > N) prefetch_l2(base_e + size_t(f.z - N - 1) * (VEC * 8) + lane * 128);
-      }
       issue(d, 0);
       cp_commit();
       // the root's pre-partial is pi
@@ -337,13 +329,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
             winn = i + 33 + lane < n ? p.pre[i + 33 + lane] : make_int4(0, 0, 0, 0);
           }
           dn = shfl4(win, li);
-        }
-        if (pf > 0 && i + pf < n) {
-          // win holds the 32 steps from (i + 1) & ~31 (updated above), winn the next 32
-          const int k = i + pf, base = (i + 1) & ~31;
-          const int4 f = shfl4(k - base < 32 ? win : winn, k & 31);
-          if (f.y > N) prefetch_l2(base_e + size_t(f.y - N - 1) * (VEC * 8) + lane * 128);
-          if (f.z > N) prefetch_l2(base_e + size_t(f.z - N - 1) * (VEC * 8) + lane * 128);
         }
         cpa_wait_all();
         __syncwarp();
