@@ -12,7 +12,8 @@
 //  * one shared-memory stage per warp: slots Q (the step's pre-partial, or
 //    the post-order edge message handed to the next step), A and B (the
 //    children's staged edge messages, or a tip child's Q P table), two TC
-//    blocks and the tip code rows (13.8 KB per warp, 128-byte aligned);
+//    blocks (13.6 KB per warp, 128-byte aligned); tip codes go straight to
+//    registers;
 //  * results are written in place: a post-order step's edge message goes to
 //    slot Q category by category after that category's operands are read, a
 //    pre-order step's outgoing pre-partial for the child visited next
@@ -49,9 +50,9 @@ struct Walk4SGeom {
   static constexpr int TCC = TCB / 2;      // double2 chunks per TC block
   static constexpr int VEC = 32 * L * MP;  // doubles per node slot of one warp
   static constexpr int SD2 = VEC / 2;      // double2 per node slot
-  // per warp: slots Q, A, B; TC blocks 0, 1; code rows (2 x 32 B); exponent row (32 ints)
+  // per warp: slots Q, A, B; TC blocks 0, 1; exponent row (32 ints)
   // (rounded up to 128 bytes: a 64-byte offset makes every 512-byte slot access 5 wavefronts)
-  static constexpr int WARP = (3 * SD2 + 2 * TCC + 4 + 8 + 7) & ~7;  // double2
+  static constexpr int WARP = (3 * SD2 + 2 * TCC + 8 + 7) & ~7;  // double2
 };
 
 template <bool HOMOG, bool HESS, int NC>
@@ -74,8 +75,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
   double2* const sB = wsm + 2 * SD2;
   double2* const sT0 = wsm + 3 * SD2;
   double2* const sT1 = sT0 + TCC;
-  double2* const sC = sT1 + TCC;  // code rows: [0..1] child 0, [2..3] child 1
-  double2* const sX = sC + 4;     // exponent row of a staged pre-partial
+  double2* const sX = sT1 + TCC;  // exponent row of a staged pre-partial
 
   const size_t wbase = size_t(warp) * size_t(N - 1);
   const double2* Eb = reinterpret_cast<const double2*>(p.escr + wbase * VEC) + lane - size_t(SD2) * size_t(N + 1);
