@@ -31,8 +31,9 @@
 //    ahead (C3 145.2 / 146.8 / 147.7 ms at distance 0 / 2 / 3), and the step
 //    list in the kernel parameters (constant bank) instead of the shuffled
 //    register window (133.0 / 133.4 vs 133.7 / 132.8 ms).
-// Arithmetic and operation order per value are walk4_kernel's, so results are
-// bit-identical to it.
+// The per-pattern arithmetic is walk4_kernel's; the warp and grid reductions
+// run in another fixed order (warp_sum2, twice the accumulator rows), so the
+// two agree to rounding and each is bit-reproducible run to run.
 #pragma once
 
 #include "pg_walk4.cuh"
