@@ -196,3 +196,33 @@ def test_walkl_small_pattern_counts(sites, monkeypatch):
     eng.invalidate_caches()
     rep2 = eng.branch_gradient(True)
     assert rep2.log_likelihood == rep.log_likelihood and np.array_equal(rep2.branch_gradient, rep.branch_gradient)
+
+
+def test_walk4s_table_width_and_kernel_agree(monkeypatch):
+    """A gapless 4-state alignment runs walk4s with 4-column TC blocks; the
+    5-column blocks (PG_WALK4S_NC5=1) and walk4 (PG_WALK4S=0) give the same
+    result to rounding, and all match the oracle (C3 model family, clock
+    rates, Hessian)."""
+    inst = synth.generate("C3", seed=21, sites=40000, tips=192)
+    assert int(inst.codes.min()) >= 0  # no missing / ambiguous codes
+    monkeypatch.setenv("PG_WALKL", "0")
+    monkeypatch.setenv("PG_WALK4_LCV", "4")
+    reps = {}
+    for name, env in (("nc4", {}), ("nc5", {"PG_WALK4S_NC5": "1"}), ("walk4", {"PG_WALK4S": "0"})):
+        for k in ("PG_WALK4S_NC5", "PG_WALK4S"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        eng, ref = _instance_pair(inst)
+        reps[name] = eng.branch_gradient(True)
+        assert eng.info()["kernel"] == ("walk4_kernel" if name == "walk4" else "walk4s_kernel")
+    ll, g, h = ref.branch_gradient(True)
+    for rep in reps.values():
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    a, b = reps["nc4"], reps["nc5"]
+    # the extra zero column changes nothing but the table layout
+    assert a.log_likelihood == b.log_likelihood and np.array_equal(a.branch_gradient, b.branch_gradient)
+    np.testing.assert_allclose(reps["walk4"].branch_gradient, a.branch_gradient, rtol=1e-12,
+                               atol=1e-14 * np.abs(a.branch_gradient).max())
