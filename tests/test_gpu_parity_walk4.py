@@ -226,3 +226,20 @@ def test_walk4s_table_width_and_kernel_agree(monkeypatch):
     assert a.log_likelihood == b.log_likelihood and np.array_equal(a.branch_gradient, b.branch_gradient)
     np.testing.assert_allclose(reps["walk4"].branch_gradient, a.branch_gradient, rtol=1e-12,
                                atol=1e-14 * np.abs(a.branch_gradient).max())
+
+
+def test_walk4_deep_caterpillar(lcv):
+    """A 700-taxon caterpillar whose site likelihoods underflow double
+    precision without rescaling (test_engine.cpp:341-361), through every
+    4-state kernel variant: the pre-partials' exponents (consumer-side scaling
+    in walk4s, per-quad normalisation in walk4t) over 700 levels."""
+    from tests.test_gpu_parity_walkm import _caterpillar_pair
+
+    eng, ref = _caterpillar_pair(4, 4, 700, 6000, 35, 0.3)
+    ll, g, h = ref.branch_gradient(True)
+    assert ll < -5000.0
+    rep = eng.branch_gradient(True)
+    assert eng.info()["kernel"] == lcv[0]
+    assert_logl(rep.log_likelihood, ll)
+    assert_vec(rep.branch_gradient, g)
+    assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
