@@ -20,8 +20,10 @@
 // load per lane.  Per-pattern quantities (normalisation peak, the gradient
 // denominator and numerators, the root mixture) are quad reductions.
 //
-// Measured (C3 full size, profiles/r23_walk4t_C3_100k*): 215.6 ms vs walk4s's
-// 145.5 ms, parity exact -- 7.4 G vs 6.5 G instructions per 10^5 columns: the
+// Measured (C3 full size, profiles/r23_walk4t_C3_100k*): 215.6 ms at 168
+// registers (3 CTAs/SM, spilling: 754 M local loads per evaluation), 185.3 ms
+// at 255 (2 CTAs/SM, the default here) vs walk4s's 138 ms, parity exact --
+// 7.4 G vs 6.5 G instructions per 10^5 columns: the
 // quad reductions (normalisation peak, denominator, numerators, root
 // mixture), the zero-initialised DMMA accumulators and the per-group
 // normalisation add back more than the mat-vecs save, and DMMA is 4 % of the
@@ -37,7 +39,7 @@
 #include "pg_walk4s.cuh"
 
 #ifndef PG_WALK4T_MINB
-#define PG_WALK4T_MINB 3
+#define PG_WALK4T_MINB 2
 #endif
 
 namespace pgk {
