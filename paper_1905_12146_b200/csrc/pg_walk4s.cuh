@@ -11,7 +11,7 @@
 // for warps:
 //  * one shared-memory stage per warp: slots Q (the step's pre-partial, or
 //    the post-order edge message handed to the next step), A and B (the
-//    children's staged edge messages, or a tip child's Q P table), two TC
+//    children's staged edge messages), two TC
 //    blocks (13.6 KB per warp, 128-byte aligned); tip codes go straight to
 //    registers;
 //  * results are written in place: a post-order step's edge message goes to
@@ -285,8 +285,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     {
       // the step's pre-partial is in slot Q: handed on in place by the
       // previous step (scale in qs_next) or staged from its scratch slot with
-      // its exponent row; child 0 -> TC 0 + slot A (edge message, or a tip's
-      // Q P table) + code row 0; child 1 -> TC 1, slot B, code row 1
+      // its exponent row; child 0 -> TC 0 + slot A (its edge message when
+      // internal; a tip needs only its TC block and code); child 1 -> TC 1,
+      // slot B
       auto issue = [&](const int4 d, int handed) {
         if (d.x != root && handed != d.x) {
           stage_slot(sQ, Qw + size_t(d.x) * SD2);
@@ -294,13 +295,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         }
         if (d.y <= N) {
           cn0 = code_ld(d.y);
-          stage_blk(sA, p.qtc, d.y);
+
         } else {
           stage_slot_once(sA, Eb + size_t(d.y) * SD2);
         }
         if (d.z <= N) {
           cn1 = code_ld(d.z);
-          stage_blk(sB, p.qtc, d.z);
+
         } else {
           stage_slot_once(sB, Eb + size_t(d.z) * SD2);
         }
@@ -367,30 +368,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
             dd = fma(ta[r], ea[r], dd);
           }
           den = fma(PS.cw[j], dd, den);
-          // gradient numerators top . (Q e): a mat-vec for an internal child,
-          // the staged Q P column for a tip (P and Q commute, engine.hpp:260)
+          // gradient numerators top . (Q e) (engine.hpp:258-262): a 4x4
+          // mat-vec with Q from the constant bank for tips too -- cheaper here
+          // than gathering the tip's Q P column from shared memory (the
+          // shared pipe, not the fp64 pipe, bounds this kernel: C3 131.3 vs
+          // 132.8 ms with the gather)
           double qea[4], qeb[4];
-          if (a_int) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              double u = 0.0;
+          for (int r = 0; r < 4; ++r) {
+            double u = 0.0, v = 0.0;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) u = fma(qm(d.y, r, c), ea[c], u);
-              qea[r] = u;
+            for (int c = 0; c < 4; ++c) {
+              u = fma(qm(d.y, r, c), ea[c], u);
+              v = fma(qm(d.z, r, c), eb[c], v);
             }
-          } else {
-            gather_cat(sA, code0, j, qea);
-          }
-          if (b_int) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              double v = 0.0;
-#pragma unroll
-              for (int c = 0; c < 4; ++c) v = fma(qm(d.z, r, c), eb[c], v);
-              qeb[r] = v;
-            }
-          } else {
-            gather_cat(sB, code1, j, qeb);
+            qea[r] = u;
+            qeb[r] = v;
           }
           double d1a = 0.0, d1b = 0.0;
 #pragma unroll
