@@ -9,16 +9,17 @@
 // shared-memory dependency stalls with two warps per scheduler, 39 % issue
 // utilisation, memory waits ~2 % -- so this variant trades the prefetch stage
 // for warps:
-//  * one shared-memory stage per warp: slots Q (the step's pre-partial, or
-//    the post-order edge message handed to the next step), A and B (the
+//  * one shared-memory stage per warp: slots Q (the step's pre-partial), A
+//    and B (the
 //    children's staged edge messages), two TC
 //    blocks (13.6 KB per warp, 128-byte aligned); tip codes go straight to
 //    registers;
-//  * results are written in place: a post-order step's edge message goes to
-//    slot Q category by category after that category's operands are read, a
-//    pre-order step's outgoing pre-partial for the child visited next
-//    likewise, the other one to its scratch slot -- no per-lane vector
-//    arrays survive the category loop of the pre-order pass;
+//  * results are written in place: a pre-order step's outgoing pre-partial
+//    for the child visited next goes to slot Q category by category after
+//    that category's q was read, the other one to its scratch slot -- no
+//    per-lane vector arrays survive the category loop of the pre-order pass
+//    (the post-order pass, below that register peak, keeps the previous
+//    step's edge message in registers);
 //  * the pre-partials' power-of-two normalisation is applied by the consumer
 //    (the producer knows the peak only after the last category): the scale
 //    of the handed-on one travels in a register, a deferred one's exponent
@@ -154,8 +155,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     // ------------------------------------------------ post-order pass (a)
     {
       int S = 0;
-      // operands: tip -> TC block 0/1 + code row; the previous step's node ->
-      // slot Q (its edge message, written there in place); else slot A
+      // the previous step's edge message stays in registers (the post-order
+      // pass is under the pre-order pass's register peak: 127 registers,
+      // no occupancy cost; C3 128.3 / 128.7 vs 131.2 / 131.1 ms through slot Q)
+      double keep[L][4];
+      // operands: tip -> TC block 0/1 + its code (register); the previous
+      // step's node -> its edge message in registers; else slot A
       auto issue_ops = [&](const int4 d, int last) {
         if (d.y <= N) {
           cn0 = code_ld(d.y);
@@ -201,9 +206,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         for (int j = 0; j < L; ++j) {
           double a[4], b[4];
           if (ka == 0) gather_cat(sT0, code0, j, a);
-          else read_cat(ka == 1 ? sQ : sA, j, a);
+          else if (ka == 1) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = keep[j][r];
+          } else read_cat(sA, j, a);
           if (kb == 0) gather_cat(sT1, code1, j, b);
-          else read_cat(kb == 1 ? sQ : sA, j, b);
+          else if (kb == 1) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) b[r] = keep[j][r];
+          } else read_cat(sA, j, b);
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             x[j][r] = a[r] * b[r];
@@ -264,8 +275,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
               e3 = fma(b.y, xc, e3);
             }
             // in place: the kept operand of this category was read above
-            sQ[lane + (2 * j) * 32] = make_double2(e0, e1);
-            sQ[lane + (2 * j + 1) * 32] = make_double2(e2, e3);
+            keep[j][0] = e0;
+            keep[j][1] = e1;
+            keep[j][2] = e2;
+            keep[j][3] = e3;
             __stcs(dst + (2 * j) * 32, make_double2(e0, e1));
             __stcs(dst + (2 * j + 1) * 32, make_double2(e2, e3));
           }
