@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           }
         }
         __syncwarp();
-        // slot A, the TC blocks and the code rows are free: the next step's operands
+        // slot A and the TC blocks are free: the next step's operands
         if (i + 1 < n) issue_ops(dn, d.x);
         if (!p.disable) {
           const int ex = peak_exponent(hm);
