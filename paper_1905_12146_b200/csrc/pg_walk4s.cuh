@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           }
         }
         __syncwarp();
-        // the next step's operands (slots A, B, TC blocks, code rows; slot Q
+        // the next step's operands (slots A, B, TC blocks; slot Q
         // unless its pre-partial was just handed on there)
         if (i + 1 < n) issue(dn, d.w);
         cp_commit();
