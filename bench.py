@@ -61,6 +61,9 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size fixture check")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period in the timed region (0: off)")
+    ap.add_argument("--also", default=None,
+                    help="comma-separated extra workloads summarised under other_workloads after the main line is "
+                         "measured (default: C2,C4,C5 for the plain one-GPU C3 run; '' turns it off)")
     return ap.parse_args(argv)
 
 
@@ -379,6 +382,35 @@ def parity_block(args, inst, logl, grad):
     return out
 
 
+def other_workloads(args):
+    """BASELINE.json's other single-GPU configs, each measured by its own
+    `bench.py --config Cx` process after this run's engine was released (same
+    steps / warm-up, full-size parity fixture, no CPU leg), summarised so that
+    the driver's one line carries a measured number for every kernel family."""
+    out = []
+    for cfg in [c for c in args.also.split(",") if c]:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg, "--steps", str(args.steps), "--warmup",
+               str(args.warmup), "--no-cpu-baseline", "--also", "", "--clock-ms", str(args.clock_ms)]
+        t0 = time.perf_counter()
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            rf, par = d["roofline"], d.get("parity") or {}
+            out.append({
+                "workload": cfg, "patterns": d["config"]["patterns"], "branches": d["config"]["branches"],
+                "states": d["config"]["states"], "kernel": d["geometry"]["kernel"], "ms_per_step": d["ms_per_step"],
+                "value": d["value"], "e2e_value": d["e2e"]["value"], "unit": d["unit"], "steps": d["steps"],
+                "roofline": {k: rf.get(k) for k in ("bound", "achieved", "peak", "unit", "frac", "walk_ms",
+                                                      "dram_frac_of_hbm")},
+                "parity": {k: par.get(k) for k in ("fixture", "logL_rel", "grad_max_rel", "grad_max_rel_to_condition",
+                                                    "components_over_1e-9_rel", "within_1e-9")},
+                "gpu_launches": d["gpu_launches"], "sm_mhz": (d.get("clocks") or {}).get("sm_mhz"),
+                "wall_s": round(time.perf_counter() - t0, 1)})
+        except Exception as e:  # the main line must not depend on the extras
+            out.append({"workload": cfg, "error": f"{type(e).__name__}: {e}"[:300]})
+    return out
+
+
 def run_reference(args, inst):
     threads = os.cpu_count() or 1
     sample = args.cpu_sample or default_sample(inst)
@@ -576,6 +608,19 @@ def run_device(args):
                 # (engine.hpp:13-17), on a quarter of the sample
                 v1, how1 = cpu_baseline(inst, max(8, sample // 4), 1, min(args.cpu_seconds, 4.0))
                 line["cpu_baseline"]["single_thread"] = {"value": v1, "cores": 1, "sample": how1}
+        also = args.also
+        if also is None:
+            also = "C2,C4,C5" if (args.config == "C3" and world == 1 and args.sites is None) else ""
+        if also and world == 1:
+            # release this run's engine (its scratch is a fixed share of the
+            # device memory) before the other workloads' processes start
+            import gc
+
+            args.also = also
+            del eng, sh, out, step_device, step_e2e
+            gc.collect()
+            torch.cuda.empty_cache()
+            line["other_workloads"] = other_workloads(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

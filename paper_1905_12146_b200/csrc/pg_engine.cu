@@ -37,7 +37,8 @@ static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
 }
 int pg_walk4_nc(int nc);
 void* pg_walkl_kernel(int L, bool homog, bool hess);
-void* pg_walkm_kernel(int mp, bool hess);
+void* pg_walkm_kernel(int mp, bool hess, bool fast);
+bool pg_walkm_fast_tables_fit(int mp, int nc);
 size_t pg_walkm_smem(int mp);
 int pg_walkm_wpc(int mp);
 
@@ -950,8 +951,8 @@ int pg_engine::walk_max_blocks_per_sm() {
 int pg_engine::walk_max_blocks_per_sm_occ() {
   int nb = 0;
   if (use_walkm) {
-    for (int h = 0; h < 2; ++h) {
-      const void* fn = pg_walkm_kernel(MP, h != 0);
+    for (int h = 0; h < 3; ++h) {
+      const void* fn = pg_walkm_kernel(MP, h == 1, h == 2);
       PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 32 * walkm_wpc, walk_smem));
@@ -1061,7 +1062,12 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
     pm.fpt = d_fpt.p;
     pm.fq = d_fq.p;
     pm.homogeneous = branch_q.empty() ? 1 : 0;
-    void* fn = pg_walkm_kernel(MP, do_hess);
+    // the compile-time-folded gradient kernel when its assumptions hold
+    // (PG_WALKM_FAST=0 keeps the general one, for A/B)
+    static const bool fast_env = !(std::getenv("PG_WALKM_FAST") && std::atoi(std::getenv("PG_WALKM_FAST")) == 0);
+    const bool fast = fast_env && !do_hess && branch_q.empty() && !opt.disable_rescaling && L == 4 &&
+                      pg_walkm_fast_tables_fit(MP, NC);
+    void* fn = pg_walkm_kernel(MP, do_hess, fast);
     void* args[] = {&pm};
     PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / walkm_wpc)), dim3(32 * walkm_wpc), args, walk_smem, stream));
     return;

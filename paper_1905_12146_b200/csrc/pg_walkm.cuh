@@ -86,6 +86,10 @@ __device__ __forceinline__ void dmma_chain(const double (&x)[K], double (&d)[NT]
 #define PG_WALKM_WPC_SMALL 4
 #endif
 
+#ifndef PG_WALKM_WPC_LARGE
+#define PG_WALKM_WPC_LARGE 4
+#endif
+
 template <int MP>
 struct WalkMGeom {
   static_assert(MP % 4 == 0, "MP: whole k-steps");
@@ -101,7 +105,7 @@ struct WalkMGeom {
   // warps per CTA (lock-step group sharing each staged matrix).  Measured on
   // C5: 8 warps with double-buffered 32 KB codon blocks (one CTA per SM) is
   // slower than two 4-warp CTAs (432 vs 423 ms).
-  static constexpr int WPC = MP <= 32 ? PG_WALKM_WPC_SMALL : 4;
+  static constexpr int WPC = MP <= 32 ? PG_WALKM_WPC_SMALL : PG_WALKM_WPC_LARGE;
   // one (node, category) scratch slot: K x 32 doubles of the warp's 8 vectors
   // followed by their 8 int exponents (one bulk copy moves both)
   static constexpr int SL = K * 32 + 4;
@@ -118,7 +122,12 @@ struct WalkMGeom {
 
 // HESS: Hessian-diagonal variant (a template parameter so the gradient-only
 // kernel does not carry the Q^2 e terms in its register allocation)
-template <int MP, bool HESS>
+// FAST: the launch-invariant switches of the common case folded at compile
+// time -- one shared generator, rescaling on, L = 4 categories (weights and
+// rates in shared memory), operands and tip tables staged (the host checks
+// walkm_fast_ok) -- so the unit body carries no branches or index
+// multiplications for them
+template <int MP, bool HESS, bool FAST>
 __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_MINB_SMALL : 2)) walkm_kernel(const __grid_constant__ WalkMParams PM) {
   using Gm = WalkMGeom<MP>;
   constexpr int K = Gm::K, NT = Gm::NT, FRAG = Gm::FRAG;
@@ -174,7 +183,8 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   };
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int q = lane >> 2, t = lane & 3;  // pattern within the warp, state phase
-  const int N = p.N, L = p.L, root = 2 * N - 1, NC = p.NC;
+  const int N = p.N, L = FAST ? 4 : p.L, root = 2 * N - 1, NC = p.NC;
+  const bool rescale = FAST || !p.disable;
   constexpr int WPC = Gm::WPC, CT = 32 * WPC;  // warps / threads per CTA
   const int warp = blockIdx.x * WPC + wib;
   const int ntile_cta = (p.P + 8 * WPC - 1) / (8 * WPC);
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   auto matvec_P = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
   auto matvec_PT = [&](const double* buf, const double (&x)[K], double (&y)[K]) { matvec(buf, x, y); };
   // homogeneous Q staged in smem; per-branch generators read in fragment order from global
-  const bool homog = PM.homogeneous != 0;
+  const bool homog = FAST || PM.homogeneous != 0;
   // y = Q_x x for the generator of node x's branch (shared generator staged
   // in shared memory; per-branch ones in fragment order from global)
   auto matvec_Q = [&](int x_node, const double (&x)[K], double (&y)[K]) {
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
   double* pism = reinterpret_cast<double*>(mbar + 2);
   double* probsm = pism + MP;
   double* ratesm = probsm + Gm::kSmemCats;
-  const bool cats_sm = p.L <= Gm::kSmemCats;
+  const bool cats_sm = FAST || p.L <= Gm::kSmemCats;
   for (int i = tid; i < MP; i += CT) pism[i] = p.pi[i];
   if (cats_sm)
     for (int i = tid; i < p.L; i += CT) {
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     const uint8_t* codes = p.codes + sc;
     const int Pc = int(p.Pc);
     const int n = p.nsteps, U = n * L;
-    const bool sop = Gm::SOP && L > 1;
+    const bool sop = Gm::SOP && (FAST || L > 1);
 
     // slot layout: [category][k-step pair][lane] double2 (512 B per warp access),
     // an odd last k-step as [lane] double, then the 8 patterns' exponents
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
     // a tip operand: the child's whole column table (NC x MP) is one bulk copy
     // into the operand's CTA region when it fits (each lane then reads its
     // pattern's column); otherwise per-lane 8-byte gathers of the column
-    const bool tstage = Gm::SOP && NC * MP <= WPC * SL;
+    const bool tstage = Gm::SOP && (FAST || NC * MP <= WPC * SL);
     auto opblk = [&](int stage, int which) -> double* { return sop_cta + (stage * 3 + which) * WPC * SL; };
     auto stage_gather_op = [&](int stage, int which, int node, int code, int l) {
       if (tstage) {
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
         }
 #pragma unroll
         for (int ki = 0; ki < K; ++ki) a[ki] *= b[ki];
-        const int ex = p.disable ? 0 : quad_peak_exp(a);
+        const int ex = rescale ? quad_peak_exp(a) : 0;
         scale_by(a, ex);
         const int Sk = xa + xb + ex;
         if (stc.x == root) {
@@ -532,7 +542,7 @@ __global__ void __launch_bounds__(32 * WalkMGeom<MP>::WPC, (MP <= 32 ? PG_WALKM_
       // receives the child's Q P column table (NC x MP) when it fits: the
       // tip's Q e is then a shared-memory read instead of a dependent global
       // gather in the middle of the unit
-      const bool qstage = PIPE && NC * MP <= FRAG;
+      const bool qstage = PIPE && (FAST || NC * MP <= FRAG);
       auto stage_qtc = [&](double* buf, int node, int l, int sb) {
         if (tid == kPIssuer) {
           bulk_g2s(buf, p.qtc + size_t((node - 1) * L + l) * (NC * MP), NC * MP * sizeof(double), mbar + sb);
