@@ -31,6 +31,10 @@ void* pg_walk4s_kernel(bool homog, bool hess, int nc);
 void* pg_walk4t_kernel(bool hess, int nc);
 size_t pg_walk4t_smem(int nc);
 size_t pg_walk4s_smem(int nc);
+void* pg_walk4s_cherry_kernel(bool homog, bool hess);
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, double* ct, cudaStream_t stream);
+void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,
+                     cudaStream_t stream);
 static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
   if (L != 4) return pg_walk4_kernel_l12(homog, hess, nc, L);
   return lcv == 4 ? pg_walk4_kernel_lc4(homog, hess, nc) : pg_walk4_kernel_lc2(homog, hess, nc);
@@ -114,6 +118,10 @@ struct pg_engine {
   int N = 0;
   std::vector<int> parent, children;  // [2N], [2N*2]
   std::vector<int4> post_steps, pre_steps;
+  // walk4s cherry tables (pg_walk4s.cuh): {k, a, b, 0} per cherry, the step
+  // lists with the children's cherry flags (post: without the cherries' steps)
+  bool use_cherry = false;
+  std::vector<int4> cherries, post_steps_ch, pre_steps_ch;
   // patterns
   int m_aln = 0, P = 0, A = 0;
   bool classes_used = true;  // some tip code is missing (-1) or an ambiguity class
@@ -161,7 +169,9 @@ struct pg_engine {
   DevBuf<double> d_qtc, d_fpp, d_fpt, d_fq, d_f4post, d_f4pre;
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err, d_qexp;
-  DevBuf<int4> d_post, d_pre;
+  DevBuf<int4> d_post, d_pre, d_cherries;
+  DevBuf<double> d_ct;
+  DevBuf<uint8_t> d_ccodes;
   DevBuf<double> d_escr, d_qscr, d_acc, d_out, d_site_ll;
   DevBuf<double> d_cap_post, d_cap_pre;
   DevBuf<int> d_cap_post_exp, d_cap_pre_exp;
@@ -732,8 +742,45 @@ struct pg_engine {
       d_fpp.ensure(size_t(B()) * L * frag);
       d_fpt.ensure(size_t(B()) * L * frag);
     }
-    d_post.upload(post_steps.data(), post_steps.size(), stream);
-    d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
+    // cherry tables: walk4s with the 4 state columns only (no missing or
+    // ambiguous codes), an internal non-root node with two tip children
+    // (PG_WALK4S_CHERRY=0 turns them off, for A/B)
+    use_cherry = false;
+    cherries.clear();
+    if (use_walk4 && use_walk4s && NC == 4 && m == 4 && N > 2 &&
+        !(std::getenv("PG_WALK4S_CHERRY") && std::atoi(std::getenv("PG_WALK4S_CHERRY")) == 0)) {
+      std::vector<char> is_ch(size_t(2 * N), 0);
+      for (const int4& st : post_steps)
+        if (st.x != 2 * N - 1 && st.y <= N && st.z <= N) {
+          is_ch[size_t(st.x)] = 1;
+          cherries.push_back(make_int4(st.x, st.y, st.z, 0));
+        }
+      use_cherry = !cherries.empty();
+      if (use_cherry) {
+        auto flagged = [&](int4 st) {
+          if (st.y > N && is_ch[size_t(st.y)]) st.x |= pgk::kCherryY;
+          if (st.z > N && is_ch[size_t(st.z)]) st.x |= pgk::kCherryZ;
+          return st;
+        };
+        post_steps_ch.clear();
+        pre_steps_ch.clear();
+        for (const int4& st : post_steps)
+          if (!is_ch[size_t(st.x)]) post_steps_ch.push_back(flagged(st));
+        for (const int4& st : pre_steps) pre_steps_ch.push_back(flagged(st));
+        d_cherries.upload(cherries.data(), cherries.size(), stream);
+        d_ct.ensure(size_t(N - 1) * 256);
+        d_ccodes.ensure(size_t(N - 1) * size_t(Pc));
+        pg_cherry_codes(d_cherries.p, int(cherries.size()), N, Pc, d_codes.p, d_ccodes.p, stream);
+        PG_CUDA(cudaGetLastError());
+      }
+    }
+    if (use_cherry) {
+      d_post.upload(post_steps_ch.data(), post_steps_ch.size(), stream);
+      d_pre.upload(pre_steps_ch.data(), pre_steps_ch.size(), stream);
+    } else {
+      d_post.upload(post_steps.data(), post_steps.size(), stream);
+      d_pre.upload(pre_steps.data(), pre_steps.size(), stream);
+    }
     if (!h_out) {
       PG_CUDA(cudaMallocHost(&h_err, 3 * sizeof(int)));
       PG_CUDA(cudaEventCreate(&ev0));
@@ -798,6 +845,11 @@ struct pg_engine {
     if (tc_dirty) {
       launch_tc();
       ++launches;
+      if (use_cherry) {
+        pg_cherry_tables(d_cherries.p, int(cherries.size()), N, d_tc.p, d_ct.p, stream);
+        PG_CUDA(cudaGetLastError());
+        ++launches;
+      }
       tc_dirty = false;
     }
     PG_CUDA(cudaEventRecord(ev1, stream));
@@ -978,6 +1030,13 @@ int pg_engine::walk_max_blocks_per_sm_occ() {
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
       nb = v == 0 ? b : std::min(nb, b);
+      if (use_walk4s && NC == 4) {
+        // the cherry-table instances share the grid (decided before the cherries are known)
+        const void* fc = pg_walk4s_cherry_kernel(branch_q.empty(), v & 1);
+        PG_CUDA(cudaFuncSetAttribute(fc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fc, pgk::kWarpsPerBlock * 32, walk_smem));
+        nb = std::min(nb, b);
+      }
     }
   } else {
     PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_walk(MP, LC), pgk::kWarpsPerBlock * 32, 0));
@@ -1124,7 +1183,11 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
                                  walk_smem, stream));
         return;
       }
-      void* fn = pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
+      ps.ct = use_cherry ? d_ct.p : nullptr;
+      ps.ccodes = use_cherry ? d_ccodes.p : nullptr;
+      ps.npost = use_cherry ? int(post_steps_ch.size()) : int(post_steps.size());
+      void* fn = use_cherry ? pg_walk4s_cherry_kernel(branch_q.empty(), do_hess)
+                            : pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
       void* args[] = {&ps};
       PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,
                                walk_smem, stream));

@@ -119,11 +119,18 @@ struct Walk4Params {
   double pi[4];
 };
 
+// cherry flags of a step's children in its descriptor's x (pg_walk4s.cuh, CH instances)
+constexpr int kCherryY = 1 << 29, kCherryZ = 1 << 30, kNodeMask = kCherryY - 1;
+
 // Parameters of the single-buffered 4-state kernel (pg_walk4s.cuh).
 struct Walk4SParams {
   Walk4Params w;
   double cw[4], crw[4], cr2w[4];  // category weights w_l, c_l w_l, c_l^2 w_l (constant-bank operands)
   int* qexp;                       // [TW][N-1][32] normalisation exponents of the deferred pre-partials
+  // cherry tables (pg_walk4s.cuh, CH instances)
+  const double* ct;       // [N-1][4][16][4] e_k per (category, code pair) of cherry node k, by k - N - 1
+  const uint8_t* ccodes;  // [N-1][Pc] combined code rows 4 ca + cb, by k - N - 1
+  int npost;              // post-order steps without the cherries' own
 };
 
 // Parameters of the tensor-core 4-state kernel (pg_walk4t.cuh).

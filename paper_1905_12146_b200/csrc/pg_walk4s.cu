@@ -2,10 +2,31 @@
 // categories, one lane per pattern, homogeneous / per-branch generators x
 // with / without the Hessian x TC column counts NC in {4 (no missing /
 // ambiguous codes), 5, 16}.
+#include <algorithm>
+
 #include "pg_walk4s.cuh"
 
 #define PG_W4S(H, S, NC) \
   if (homog == H && hess == S && nc == NC) return reinterpret_cast<void*>(&pgk::walk4s_kernel<H, S, NC>);
+
+// cherry-table instances (NC = 4)
+void* pg_walk4s_cherry_kernel(bool homog, bool hess) {
+  if (homog) return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<true, true, 4, true>)
+                         : reinterpret_cast<void*>(&pgk::walk4s_kernel<true, false, 4, true>);
+  return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<false, true, 4, true>)
+              : reinterpret_cast<void*>(&pgk::walk4s_kernel<false, false, 4, true>);
+}
+
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, double* ct, cudaStream_t stream) {
+  if (ncherry > 0) pgk::cherry_tc_kernel<<<(ncherry * 64 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, ct);
+}
+
+void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,
+                     cudaStream_t stream) {
+  if (ncherry <= 0) return;
+  const unsigned gx = unsigned(std::min<long long>((Pc + 255) / 256, 64));
+  pgk::cherry_codes_kernel<<<dim3(gx, unsigned(ncherry)), 256, 0, stream>>>(cherries, ncherry, N, Pc, codes, cc);
+}
 
 void* pg_walk4s_kernel(bool homog, bool hess, int nc) {
   PG_W4S(true, false, 4)

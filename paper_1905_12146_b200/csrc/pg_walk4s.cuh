@@ -57,9 +57,55 @@ struct Walk4SGeom {
   static constexpr int WARP = (3 * SD2 + 2 * TCC + 8 + 7) & ~7;  // double2
 };
 
-template <bool HOMOG, bool HESS, int NC>
+// Cherry tables (CH instances; NC = 4, no missing / ambiguous tip codes): the
+// edge message of a cherry -- an internal node whose two children are tips --
+// depends on its pattern only through the two tip codes, so K1's epilogue
+// (cherry_tc_kernel) tabulates e_k = P_k (P_a[:, ca] o P_b[:, cb]) for the 16
+// code pairs and the cherry becomes a "tip" with 16 columns, addressed by the
+// combined code row 4 ca + cb: its post-order step, its stored edge message
+// (a third of the edge scratch traffic on a Yule tree) and the 4 KB operand
+// copy of its parent's pre-order step disappear; the parent stages the 2 KB
+// table into a free operand slot and gathers.  The table is left unnormalised
+// (the parent's own power-of-two normalisation absorbs the scale exactly).
+// Step descriptors carry the children's cherry flags in bits 29 / 30 of x.
+
+// one thread per (cherry, category, code pair); TC is [B][4][4][4]
+static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int ncherry, int N, const double* __restrict__ tc,
+                                 double* __restrict__ ct) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncherry * 64) return;
+  const int ci = i >> 6, l = (i >> 4) & 3, combo = i & 15;
+  const int4 ch = cherries[ci];  // {k, a, b, 0}
+  const double* Ta = tc + (size_t(ch.y - 1) * 4 + l) * 16 + (combo >> 2) * 4;
+  const double* Tb = tc + (size_t(ch.z - 1) * 4 + l) * 16 + (combo & 3) * 4;
+  const double* Tk = tc + (size_t(ch.x - 1) * 4 + l) * 16;
+  double e[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double xc = Ta[c] * Tb[c];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) e[r] = fma(Tk[c * 4 + r], xc, e[r]);
+  }
+  double* out = ct + (size_t(ch.x - N - 1) * 4 + l) * 64 + combo * 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) out[r] = e[r];
+}
+
+// combined code rows of the cherries: cc[k - N - 1][s] = 4 code_a[s] + code_b[s]
+static __global__ void cherry_codes_kernel(const int4* __restrict__ cherries, int ncherry, int N, long long Pc,
+                                    const uint8_t* __restrict__ codes, uint8_t* __restrict__ cc) {
+  const int4 ch = cherries[blockIdx.y];
+  const uint8_t* a = codes + size_t(ch.y - 1) * Pc;
+  const uint8_t* b = codes + size_t(ch.z - 1) * Pc;
+  uint8_t* o = cc + size_t(ch.x - N - 1) * Pc;
+  for (long long s = blockIdx.x * blockDim.x + threadIdx.x; s < Pc; s += (long long)gridDim.x * blockDim.x)
+    o[s] = uint8_t(4 * (a[s] & 3) + (b[s] & 3));
+}
+
+template <bool HOMOG, bool HESS, int NC, bool CH = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     walk4s_kernel(const __grid_constant__ Walk4SParams PS) {
+  static_assert(!CH || NC == 4, "cherry tables: 4 x 4 code pairs");
   using Gm = Walk4SGeom<NC>;
   constexpr int L = 4, TCC = Gm::TCC, VEC = Gm::VEC, SD2 = Gm::SD2;
   static_assert(TCC <= SD2, "a TC block fits in an operand slot");
@@ -124,6 +170,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     v[2] = b.x;
     v[3] = b.y;
   };
+  // a cherry's table [category][code pair][4] staged in an operand slot
+  auto gather_ct = [&](const double2* tbl, int code, int j, double (&v)[4]) {
+    const double2* c = tbl + (j * 16 + code) * 2;
+    const double2 a = c[0], b = c[1];
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  };
+  auto stage_ct = [&](double2* d, int node) {
+    const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * 128 + lane;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
+  };
+  // descriptor -> node ids + the children's cherry flags (bit 0: y, bit 1: z)
+  auto unflag = [&](int4& d) -> int {
+    if constexpr (!CH) return 0;
+    const int f = (d.x >> 29) & 3;
+    d.x &= kNodeMask;
+    return f;
+  };
   auto qm = [&](int x, int r, int c) -> double {
     if constexpr (HOMOG) return P4.q[r * 4 + c];
     else return __ldg(p.qtab + size_t(p.qidx[x]) * 16 + r * 4 + c);
@@ -150,6 +217,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     // step is issued (consumed one step later; cheaper than staging the
     // 32-byte row through shared memory: C3 18 instructions per step)
     auto code_ld = [&](int tip) -> int { return __ldg(codes + size_t(tip - 1) * Pc + lane); };
+    // a cherry's combined code 4 ca + cb ([N-1][Pc] rows by node - N - 1)
+    const uint8_t* ccodes = CH ? PS.ccodes + size_t(t) * 32 : nullptr;
+    auto ccode_ld = [&](int node) -> int { return __ldg(ccodes + size_t(node - N - 1) * Pc + lane); };
     int cn0 = 0, cn1 = 0;  // the next step's tip codes
 
     // ------------------------------------------------ post-order pass (a)
@@ -161,14 +231,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       double keep[L][4];
       // operands: tip -> TC block 0/1 + its code (register); the previous
       // step's node -> its edge message in registers; else slot A
-      auto issue_ops = [&](const int4 d, int last) {
-        if (d.y <= N) {
+      // (CH) a cherry child: its combined code + its table into slot Q
+      // (child 0; unused by this pass) or behind the node's own block in slot B
+      auto issue_ops = [&](const int4 d, int f, int last) {
+        if (CH && (f & 1)) {
+          cn0 = ccode_ld(d.y);
+          stage_ct(sQ, d.y);
+        } else if (d.y <= N) {
           cn0 = code_ld(d.y);
           stage_blk(sT0, p.tc, d.y);
         } else if (d.y != last) {
           stage_slot(sA, Eb + size_t(d.y) * SD2);
         }
-        if (d.z <= N) {
+        if (CH && (f & 2)) {
+          cn1 = ccode_ld(d.z);
+          stage_ct(sB + TCC, d.z);
+        } else if (d.z <= N) {
           cn1 = code_ld(d.z);
           stage_blk(sT1, p.tc, d.z);
         } else if (d.z != last) {
@@ -178,15 +256,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       auto issue_own = [&](const int4 d) {
         if (d.x != root) stage_blk(sB, p.tc, d.x);
       };
+      const int n = CH ? PS.npost : p.nsteps;  // (CH) the cherries' own steps are gone
       int4 win = lane < n ? p.post[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.post[32 + lane] : make_int4(0, 0, 0, 0);
       int4 d = shfl4(win, 0);
-      issue_ops(d, -1);
+      int f = unflag(d);
+      issue_ops(d, f, -1);
       issue_own(d);
       cp_commit();
       int last = -1;
       for (int i = 0; i < n; ++i) {
         int4 dn = make_int4(0, 0, 0, 0);
+        int fn = 0;
         if (i + 1 < n) {
           const int li = (i + 1) & 31;
           if (li == 0) {
@@ -194,23 +275,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
             winn = i + 33 + lane < n ? p.post[i + 33 + lane] : make_int4(0, 0, 0, 0);
           }
           dn = shfl4(win, li);
+          fn = unflag(dn);
         }
         cpa_wait_all();
         __syncwarp();
-        const int ka = d.y <= N ? 0 : d.y == last ? 1 : 2;
-        const int kb = d.z <= N ? 0 : d.z == last ? 1 : 2;
+        const int ka = (CH && (f & 1)) ? 3 : d.y <= N ? 0 : d.y == last ? 1 : 2;
+        const int kb = (CH && (f & 2)) ? 3 : d.z <= N ? 0 : d.z == last ? 1 : 2;
         const int code0 = cn0, code1 = cn1;
         double x[L][4];
         int hm = 0;
 #pragma unroll
         for (int j = 0; j < L; ++j) {
           double a[4], b[4];
-          if (ka == 0) gather_cat(sT0, code0, j, a);
+          if (ka == 3) gather_ct(sQ, code0, j, a);
+          else if (ka == 0) gather_cat(sT0, code0, j, a);
           else if (ka == 1) {
 #pragma unroll
             for (int r = 0; r < 4; ++r) a[r] = keep[j][r];
           } else read_cat(sA, j, a);
-          if (kb == 0) gather_cat(sT1, code1, j, b);
+          if (kb == 3) gather_ct(sB + TCC, code1, j, b);
+          else if (kb == 0) gather_cat(sT1, code1, j, b);
           else if (kb == 1) {
 #pragma unroll
             for (int r = 0; r < 4; ++r) b[r] = keep[j][r];
@@ -223,7 +307,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         }
         __syncwarp();
         // slot A and the TC blocks are free: the next step's operands
-        if (i + 1 < n) issue_ops(dn, d.x);
+        if (i + 1 < n) issue_ops(dn, fn, d.x);
         if (!p.disable) {
           const int ex = peak_exponent(hm);
           if (ex != 0) {
@@ -288,6 +372,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         if (i + 1 < n) issue_own(dn);
         cp_commit();
         d = dn;
+        f = fn;
       }
       cpa_wait_all();
       __syncwarp();
@@ -301,20 +386,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       // its exponent row; child 0 -> TC 0 + slot A (its edge message when
       // internal; a tip needs only its TC block and code); child 1 -> TC 1,
       // slot B
-      auto issue = [&](const int4 d, int handed) {
+      // (CH) a cherry child's edge message: its table in the slot + its combined code
+      auto issue = [&](const int4 d, int f, int handed) {
         if (d.x != root && handed != d.x) {
           stage_slot(sQ, Qw + size_t(d.x) * SD2);
           if (lane < 8) cp16_cg(sX + lane, Xb + size_t(d.x) * 32 + 4 * lane);
         }
         if (d.y <= N) {
           cn0 = code_ld(d.y);
-
+        } else if (CH && (f & 1)) {
+          cn0 = ccode_ld(d.y);
+          stage_ct(sA, d.y);
         } else {
           stage_slot_once(sA, Eb + size_t(d.y) * SD2);
         }
         if (d.z <= N) {
           cn1 = code_ld(d.z);
-
+        } else if (CH && (f & 2)) {
+          cn1 = ccode_ld(d.z);
+          stage_ct(sB, d.z);
         } else {
           stage_slot_once(sB, Eb + size_t(d.z) * SD2);
         }
@@ -325,7 +415,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
       int4 d = shfl4(win, 0);
-      issue(d, 0);
+      int f = unflag(d);
+      issue(d, f, 0);
       cp_commit();
       // the root's pre-partial is pi
 #pragma unroll
@@ -337,6 +428,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
       int handed = 0;
       for (int i = 0; i < n; ++i) {
         int4 dn = make_int4(0, 0, 0, 0);
+        int fn = 0;
         if (i + 1 < n) {
           const int li = (i + 1) & 31;
           if (li == 0) {
@@ -344,6 +436,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
             winn = i + 33 + lane < n ? p.pre[i + 33 + lane] : make_int4(0, 0, 0, 0);
           }
           dn = shfl4(win, li);
+          fn = unflag(dn);
         }
         cpa_wait_all();
         __syncwarp();
@@ -351,12 +444,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         else if (handed == d.x) qs = qs_next;
         else qs = qscale(reinterpret_cast<const int*>(sX)[lane]);
         const bool a_int = d.y > N, b_int = d.z > N;
+        const bool a_ch = CH && (f & 1), b_ch = CH && (f & 2);
         const int code0 = cn0, code1 = cn1;
         // consumed scratch is dead: drop it from L2 without write-back
         if (lane < VEC / 16) {
           const char* base_q = reinterpret_cast<const char*>(p.qscr + wbase * VEC);
-          if (a_int) discard_l2(base_e + size_t(d.y - N - 1) * (VEC * 8) + lane * 128);
-          if (b_int) discard_l2(base_e + size_t(d.z - N - 1) * (VEC * 8) + lane * 128);
+          if (a_int && !a_ch) discard_l2(base_e + size_t(d.y - N - 1) * (VEC * 8) + lane * 128);
+          if (b_int && !b_ch) discard_l2(base_e + size_t(d.z - N - 1) * (VEC * 8) + lane * 128);
           if (d.x != root && handed != d.x) discard_l2(base_q + size_t(d.x - N - 1) * (VEC * 8) + lane * 128);
         }
         double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
@@ -369,9 +463,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           read_cat(sQ, j, q);
 #pragma unroll
           for (int r = 0; r < 4; ++r) q[r] *= qs;
-          if (a_int) read_cat(sA, j, ea);
+          if (a_ch) gather_ct(sA, code0, j, ea);
+          else if (a_int) read_cat(sA, j, ea);
           else gather_cat(sT0, code0, j, ea);
-          if (b_int) read_cat(sB, j, eb);
+          if (b_ch) gather_ct(sB, code1, j, eb);
+          else if (b_int) read_cat(sB, j, eb);
           else gather_cat(sT1, code1, j, eb);
           double ta[4], tb[4], dd = 0.0;
 #pragma unroll
@@ -459,7 +555,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         __syncwarp();
         // the next step's operands (slots A, B, TC blocks; slot Q
         // unless its pre-partial was just handed on there)
-        if (i + 1 < n) issue(dn, d.w);
+        if (i + 1 < n) issue(dn, fn, d.w);
         cp_commit();
         const double inv = 1.0 / den;
         {
@@ -486,6 +582,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         }
         handed = d.w;
         d = dn;
+        f = fn;
       }
       cpa_wait_all();
       __syncwarp();
