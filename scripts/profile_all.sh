@@ -11,7 +11,7 @@ for cfg in ${CONFIGS:-C3 C2 C4 C5}; do
   ncu --set full --clock-control none --import-source on -k regex:walk -s 1 -c 1 -o gpurun_out/walk_${TAG}_$cfg -f $CMD > gpurun_out/ncu_${TAG}_$cfg.log 2>&1
   echo "$cfg rc=$?"; tail -1 gpurun_out/pf_${TAG}_$cfg.log
 done
-BCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+BCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --also \"\""
 $BCMD > gpurun_out/bench_plain_${TAG}.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench_${TAG}.csv $BCMD > gpurun_out/ncu_launch_bench_${TAG}.log 2>&1
 echo "launch list rc=$?"

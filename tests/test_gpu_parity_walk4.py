@@ -243,3 +243,94 @@ def test_walk4_deep_caterpillar(lcv):
     assert_logl(rep.log_likelihood, ll)
     assert_vec(rep.branch_gradient, g)
     assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+
+
+def _newick_pair(newick, sites, seed, hess_model_seed=3, branch_q=False):
+    """Engine + oracle on a Newick tree with simulated gapless 4-state data
+    (non-reversible generator, Γ4) and enough patterns for walk4s."""
+    rng = np.random.default_rng(hess_model_seed)
+    q = rng.uniform(0.2, 1.5, (4, 4))
+    np.fill_diagonal(q, 0.0)
+    np.fill_diagonal(q, -q.sum(1))
+    pi = np.array([0.3, 0.2, 0.2, 0.3])
+    tree_o = O.Tree.parse(newick)
+    mo = O.Model(q, pi, False)
+    rates, probs = O.discrete_gamma(0.5, 4)
+    codes = O.simulate_states(tree_o, mo, rates, probs, tree_o.branch_lengths, sites, seed)
+    labels = [tree_o.labels[i] for i in range(1, tree_o.tip_count + 1)]
+    model = SubstitutionModel(q, pi, False)
+    if branch_q:
+        for br, qb in _branch_q(7, len(tree_o.branch_lengths), k=3):
+            mo.set_branch_generator(br, qb)
+            model.set_branch_generator(br, qb)
+    ref = O.Engine(tree_o, O.Alignment.from_codes(codes, 4, labels), mo, rates, probs)
+    ref._keep = (tree_o, mo)
+    tree = Tree(tree_o.tip_count, tree_o.parent, tree_o.children,
+                np.concatenate([[0.0], tree_o.branch_lengths, [0.0]]), tree_o.labels, tree_o.post_order)
+    eng = LikelihoodEngine(tree, SitePatternAlignment.from_codes(labels, codes, 4), model,
+                           RateCategories(np.asarray(rates), np.asarray(probs)), EngineOptions())
+    return eng, ref
+
+
+def _balanced(depth, rng, prefix="t"):
+    if depth == 0:
+        return f"{prefix}:{rng.uniform(0.02, 0.3):.6f}"
+    return (f"({_balanced(depth - 1, rng, prefix + 'a')},{_balanced(depth - 1, rng, prefix + 'b')})"
+            f":{rng.uniform(0.02, 0.3):.6f}")
+
+
+def _caterpillar_newick(tips, rng):
+    s = f"(c0:{rng.uniform(0.02, 0.3):.6f},c1:{rng.uniform(0.02, 0.3):.6f})"
+    for i in range(2, tips):
+        s = f"({s}:{rng.uniform(0.02, 0.3):.6f},c{i}:{rng.uniform(0.02, 0.3):.6f})"
+    return s + ";"
+
+
+@pytest.mark.parametrize("shape", ["balanced", "caterpillar", "root_cherry", "mixed"])
+@pytest.mark.parametrize("branch_q", [False, True], ids=["homog", "per_branch_q"])
+def test_walk4s_cherry_tables(shape, branch_q, monkeypatch):
+    """walk4s with cherry tables (a node with two tip children tabulated per
+    code pair, pg_walk4s.cuh CH instances) against the oracle and against the
+    same kernel without them, with the Hessian: a balanced tree (every tip in a
+    cherry, parents of two cherries), a caterpillar (one cherry at the
+    bottom), a small tree with a cherry directly under the root and a random
+    Yule tree."""
+    rng = np.random.default_rng(11)
+    if shape == "balanced":
+        nw = _balanced(6, rng)
+        nw = nw[:nw.rfind(":")] + ";"
+    elif shape == "caterpillar":
+        nw = _caterpillar_newick(40, rng)
+    elif shape == "root_cherry":
+        nw = ("((x:0.11,y:0.07):0.05,((((a:0.2,b:0.1):0.07,c:0.3):0.04,(d:0.12,(e:0.08,f:0.25):0.1):0.06):0.09,"
+              "(g:0.3,(h:0.1,(i:0.2,j:0.15):0.05):0.1):0.2):0.13);")
+    else:
+        inst = synth.generate("C3", seed=5, sites=30000, tips=100)
+        nw = None
+    monkeypatch.setenv("PG_WALKL", "0")
+    monkeypatch.setenv("PG_WALK4_LCV", "4")
+    monkeypatch.setenv("PG_WALK4S", "1")
+    reps = {}
+    for ch in ("1", "0"):
+        monkeypatch.setenv("PG_WALK4S_CHERRY", ch)
+        if nw is None:
+            eng, ref = _instance_pair(inst, _branch_q(3, inst.branches) if branch_q else ())
+        else:
+            eng, ref = _newick_pair(nw, 30000, 17, branch_q=branch_q)
+        reps[ch] = eng.branch_gradient(True)
+        assert eng.info()["kernel"] == "walk4s_kernel"
+        # K1 + cherry tables + walk + reduce with the tables, K1 + walk + reduce without
+        assert eng.info()["launches"] == (4 if ch == "1" else 3)
+    ll, g, h = ref.branch_gradient(True)
+    for rep in reps.values():
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    a, b = reps["1"], reps["0"]
+    np.testing.assert_allclose(a.log_likelihood, b.log_likelihood, rtol=1e-14)
+    np.testing.assert_allclose(a.branch_gradient, b.branch_gradient, rtol=1e-11,
+                               atol=1e-13 * np.abs(b.branch_gradient).max())
+    # the logL-only route runs the post-order pass alone
+    monkeypatch.setenv("PG_WALK4S_CHERRY", "1")
+    eng, ref = (_instance_pair(inst) if nw is None else _newick_pair(nw, 30000, 17))
+    assert_logl(eng.log_likelihood(), ref.branch_gradient(False)[0])
