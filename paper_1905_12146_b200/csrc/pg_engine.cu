@@ -121,7 +121,7 @@ struct pg_engine {
   // walk4s cherry tables (pg_walk4s.cuh): {k, a, b, 0} per cherry, the step
   // lists with the children's cherry flags (post: without the cherries' steps)
   bool use_cherry = false;
-  std::vector<int4> cherries, post_steps_ch, pre_steps_ch;
+  std::vector<int4> cherries, post_steps_ch, pre_steps_ch, pre_steps_fused;
   // patterns
   int m_aln = 0, P = 0, A = 0;
   bool classes_used = true;  // some tip code is missing (-1) or an ambiguity class
@@ -169,7 +169,7 @@ struct pg_engine {
   DevBuf<double> d_qtc, d_fpp, d_fpt, d_fq, d_f4post, d_f4pre;
   DevBuf<double> d_weights, d_tc, d_qtab, d_pi, d_rates, d_probs, d_blen, d_dt, d_eu, d_eui, d_ew, d_amb;
   DevBuf<int> d_qidx, d_err, d_qexp;
-  DevBuf<int4> d_post, d_pre, d_cherries;
+  DevBuf<int4> d_post, d_pre, d_pre_fused, d_cherries;
   DevBuf<double> d_ct;
   DevBuf<uint8_t> d_ccodes;
   DevBuf<double> d_escr, d_qscr, d_acc, d_out, d_site_ll;
@@ -767,8 +767,21 @@ struct pg_engine {
         for (const int4& st : post_steps)
           if (!is_ch[size_t(st.x)]) post_steps_ch.push_back(flagged(st));
         for (const int4& st : pre_steps) pre_steps_ch.push_back(flagged(st));
+        // one shared generator: the cherries' pre-order steps are fused into
+        // their parents' (reverse of the filtered post order; the hand-off
+        // target is the following step's node when it is a child)
+        pre_steps_fused.assign(post_steps_ch.rbegin(), post_steps_ch.rend());
+        for (size_t i = 0; i < pre_steps_fused.size(); ++i) {
+          int next = 0;
+          if (i + 1 < pre_steps_fused.size()) {
+            const int nx = pre_steps_fused[i + 1].x & pgk::kNodeMask;
+            if (parent[size_t(nx)] == (pre_steps_fused[i].x & pgk::kNodeMask)) next = nx;
+          }
+          pre_steps_fused[i].w = next;
+        }
+        d_pre_fused.upload(pre_steps_fused.data(), pre_steps_fused.size(), stream);
         d_cherries.upload(cherries.data(), cherries.size(), stream);
-        d_ct.ensure(size_t(N - 1) * 256);
+        d_ct.ensure(size_t(N - 1) * 2 * pgk::kCherryBlk);
         d_ccodes.ensure(size_t(N - 1) * size_t(Pc));
         pg_cherry_codes(d_cherries.p, int(cherries.size()), N, Pc, d_codes.p, d_ccodes.p, stream);
         PG_CUDA(cudaGetLastError());
@@ -1186,6 +1199,7 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       ps.ct = use_cherry ? d_ct.p : nullptr;
       ps.ccodes = use_cherry ? d_ccodes.p : nullptr;
       ps.npost = use_cherry ? int(post_steps_ch.size()) : int(post_steps.size());
+      if (use_cherry && branch_q.empty()) ps.w.p.pre = d_pre_fused.p;  // fused cherry steps (HOMOG instances)
       void* fn = use_cherry ? pg_walk4s_cherry_kernel(branch_q.empty(), do_hess)
                             : pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
       void* args[] = {&ps};

@@ -42,6 +42,13 @@
 #ifndef PG_WALK4S_MINB
 #define PG_WALK4S_MINB 4
 #endif
+// The cherry-table instances run 3 CTAs (12 warps) per SM at up to 168
+// registers: with a third of the steps and of the DRAM traffic gone, the
+// spill-free code beats the four extra warps (C3 115.0 vs 117.0 ms unfused;
+// the fused cherry steps need the registers: 111.5 ms vs 123.5 ms at 128)
+#ifndef PG_WALK4S_MINB_CH
+#define PG_WALK4S_MINB_CH 3
+#endif
 
 namespace pgk {
 
@@ -68,6 +75,13 @@ struct Walk4SGeom {
 // table into a free operand slot and gathers.  The table is left unnormalised
 // (the parent's own power-of-two normalisation absorbs the scale exactly).
 // Step descriptors carry the children's cherry flags in bits 29 / 30 of x.
+// With one shared generator (HOMOG) the cherry's pre-order step is fused into
+// its parent's as well: q_k = P_k^T top stays in registers and the two tips'
+// gradient terms are formed on the spot from their TC blocks (staged behind
+// the table: a cherry block is [e_k table 2 KB | TC_u | TC_v | tip node ids],
+// kCherryBlk double2), against the parent's own denominator (Eq. 8: q_k . (e_u
+// o e_v) = top_k . e_k) -- no hand-off or scratch round trip of q_k, no
+// normalisation, a third fewer pre-order steps.
 
 // one thread per (cherry, category, code pair); TC is [B][4][4][4]
 static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int ncherry, int N, const double* __restrict__ tc,
@@ -86,9 +100,15 @@ static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int n
 #pragma unroll
     for (int r = 0; r < 4; ++r) e[r] = fma(Tk[c * 4 + r], xc, e[r]);
   }
-  double* out = ct + (size_t(ch.x - N - 1) * 4 + l) * 64 + combo * 4;
+  double* blk = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk);
+  double* out = blk + l * 64 + combo * 4;
 #pragma unroll
   for (int r = 0; r < 4; ++r) out[r] = e[r];
+  // the tips' own TC blocks (32 double2 each) and node ids behind the table
+  const int t64 = i & 63;
+  const double2* src = reinterpret_cast<const double2*>(tc + size_t((t64 < 32 ? ch.y : ch.z) - 1) * 64) + (t64 & 31);
+  reinterpret_cast<double2*>(blk)[128 + t64] = *src;
+  if (t64 == 0) *reinterpret_cast<int4*>(blk + 2 * 192) = make_int4(ch.y, ch.z, 0, 0);
 }
 
 // combined code rows of the cherries: cc[k - N - 1][s] = 4 code_a[s] + code_b[s]
@@ -103,7 +123,7 @@ static __global__ void cherry_codes_kernel(const int4* __restrict__ cherries, in
 }
 
 template <bool HOMOG, bool HESS, int NC, bool CH = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : PG_WALK4S_MINB)
     walk4s_kernel(const __grid_constant__ Walk4SParams PS) {
   static_assert(!CH || NC == 4, "cherry tables: 4 x 4 code pairs");
   using Gm = Walk4SGeom<NC>;
@@ -180,10 +200,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
     v[3] = b.y;
   };
   auto stage_ct = [&](double2* d, int node) {
-    const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * 128 + lane;
+    const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
 #pragma unroll
     for (int c = 0; c < 4; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
   };
+  // the whole cherry block (table, the tips' TC blocks, their node ids)
+  auto stage_cb = [&](double2* d, int node) {
+    const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
+    if (lane == 0) cp16_ca(d + 192, gs + 192);
+  };
+  constexpr bool FUSE = CH && HOMOG;
   // descriptor -> node ids + the children's cherry flags (bit 0: y, bit 1: z)
   auto unflag = [&](int4& d) -> int {
     if constexpr (!CH) return 0;
@@ -396,7 +424,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           cn0 = code_ld(d.y);
         } else if (CH && (f & 1)) {
           cn0 = ccode_ld(d.y);
-          stage_ct(sA, d.y);
+          if constexpr (FUSE) stage_cb(sA, d.y);
+          else stage_ct(sA, d.y);
         } else {
           stage_slot_once(sA, Eb + size_t(d.y) * SD2);
         }
@@ -404,7 +433,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           cn1 = code_ld(d.z);
         } else if (CH && (f & 2)) {
           cn1 = ccode_ld(d.z);
-          stage_ct(sB, d.z);
+          if constexpr (FUSE) stage_cb(sB, d.z);
+          else stage_ct(sB, d.z);
         } else {
           stage_slot_once(sB, Eb + size_t(d.z) * SD2);
         }
@@ -412,6 +442,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
         stage_blk(sT1, p.tc, d.z);
       };
       const char* base_e = reinterpret_cast<const char*>(p.escr + wbase * VEC);
+      const int n = FUSE ? PS.npost : p.nsteps;  // (FUSE) the cherries' own steps are gone
       int4 win = lane < n ? p.pre[lane] : make_int4(0, 0, 0, 0);
       int4 winn = 32 + lane < n ? p.pre[32 + lane] : make_int4(0, 0, 0, 0);
       int4 d = shfl4(win, 0);
@@ -454,6 +485,50 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
           if (d.x != root && handed != d.x) discard_l2(base_q + size_t(d.x - N - 1) * (VEC * 8) + lane * 128);
         }
         double den = 0.0, na = 0.0, nb = 0.0, na2 = 0.0, nb2 = 0.0;
+        // (FUSE) a cherry child's tips u, v: gradient (and Hessian) numerators
+        double cau = 0.0, cav = 0.0, cbu = 0.0, cbv = 0.0, cau2 = 0.0, cav2 = 0.0, cbu2 = 0.0, cbv2 = 0.0;
+        const bool a_fuse = FUSE && a_ch, b_fuse = FUSE && b_ch;
+        auto fused_tips = [&](const double2* blk, int code, int j, const double (&o)[4], double& nu, double& nv,
+                              double& nu2, double& nv2) {
+          double eu[4], ev[4];
+          gather_cat(blk + 128, code >> 2, j, eu);
+          gather_cat(blk + 160, code & 3, j, ev);
+          double qu[4], qv[4], du = 0.0, dv = 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double x = 0.0, y = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              x = fma(P4.q[r * 4 + c], eu[c], x);
+              y = fma(P4.q[r * 4 + c], ev[c], y);
+            }
+            qu[r] = x;
+            qv[r] = y;
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            du = fma(o[r] * ev[r], qu[r], du);
+            dv = fma(o[r] * eu[r], qv[r], dv);
+          }
+          nu = fma(PS.crw[j], du, nu);
+          nv = fma(PS.crw[j], dv, nv);
+          if constexpr (HESS) {
+            double du2 = 0.0, dv2 = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              double x = 0.0, y = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                x = fma(P4.q[r * 4 + c], qu[c], x);
+                y = fma(P4.q[r * 4 + c], qv[c], y);
+              }
+              du2 = fma(o[r] * ev[r], x, du2);
+              dv2 = fma(o[r] * eu[r], y, dv2);
+            }
+            nu2 = fma(PS.cr2w[j], du2, nu2);
+            nv2 = fma(PS.cr2w[j], dv2, nv2);
+          }
+        };
         int ha = 0, hb = 0;
         double2* qa_dst = Qw + size_t(d.y) * SD2;  // lane offset included
         double2* qb_dst = Qw + size_t(d.z) * SD2;
@@ -530,7 +605,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
               o[c] = fma(u.x, ta[0], fma(u.y, ta[1], fma(v.x, ta[2], v.y * ta[3])));
               ha = max(ha, __double2hiint(o[c]));
             }
-            if (d.y == d.w) write_cat(sQ, j, o);
+            if (a_fuse) fused_tips(sA, code0, j, o, cau, cav, cau2, cav2);
+            else if (d.y == d.w) write_cat(sQ, j, o);
             else {
               __stcg(qa_dst + (2 * j) * 32, make_double2(o[0], o[1]));
               __stcg(qa_dst + (2 * j + 1) * 32, make_double2(o[2], o[3]));
@@ -545,13 +621,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
               o[c] = fma(u.x, tb[0], fma(u.y, tb[1], fma(v.x, tb[2], v.y * tb[3])));
               hb = max(hb, __double2hiint(o[c]));
             }
-            if (d.z == d.w) write_cat(sQ, j, o);
+            if (b_fuse) fused_tips(sB, code1, j, o, cbu, cbv, cbu2, cbv2);
+            else if (d.z == d.w) write_cat(sQ, j, o);
             else {
               __stcg(qb_dst + (2 * j) * 32, make_double2(o[0], o[1]));
               __stcg(qb_dst + (2 * j + 1) * 32, make_double2(o[2], o[3]));
             }
           }
         }
+        // (FUSE) the fused tips' node ids (lane 0: u, lane 16: v) before the slots are refilled
+        int ida = 0, idb = 0;
+        if (a_fuse) ida = reinterpret_cast<const int*>(sA + 192)[lane >> 4];
+        if (b_fuse) idb = reinterpret_cast<const int*>(sB + 192)[lane >> 4];
         __syncwarp();
         // the next step's operands (slots A, B, TC blocks; slot Q
         // unless its pre-partial was just handed on there)
@@ -568,14 +649,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PG_WALK4S_MINB)
                                         valid ? w * (nb2 * inv - r1b * r1b) : 0.0);
             if ((lane & 15) == 0) atomicAdd(A + p.B + (lane == 0 ? d.y : d.z), h2);
           }
+          if (a_fuse) {
+            const double ru = cau * inv, rv = cav * inv;
+            const double g3 = warp_sum2(valid ? w * ru : 0.0, valid ? w * rv : 0.0);
+            if ((lane & 15) == 0) atomicAdd(A + ida, g3);
+            if constexpr (HESS) {
+              const double h3 = warp_sum2(valid ? w * (cau2 * inv - ru * ru) : 0.0, valid ? w * (cav2 * inv - rv * rv) : 0.0);
+              if ((lane & 15) == 0) atomicAdd(A + p.B + ida, h3);
+            }
+          }
+          if (b_fuse) {
+            const double ru = cbu * inv, rv = cbv * inv;
+            const double g3 = warp_sum2(valid ? w * ru : 0.0, valid ? w * rv : 0.0);
+            if ((lane & 15) == 0) atomicAdd(A + idb, g3);
+            if constexpr (HESS) {
+              const double h3 = warp_sum2(valid ? w * (cbu2 * inv - ru * ru) : 0.0, valid ? w * (cbv2 * inv - rv * rv) : 0.0);
+              if ((lane & 15) == 0) atomicAdd(A + p.B + idb, h3);
+            }
+          }
         }
         // normalisation exponents of the emitted pre-partials
-        if (a_int) {
+        if (a_int && !a_fuse) {
           const int ex = peak_exponent(ha);
           if (d.y == d.w) qs_next = qscale(ex);
           else Xw[size_t(d.y) * 32] = ex;
         }
-        if (b_int) {
+        if (b_int && !b_fuse) {
           const int ex = peak_exponent(hb);
           if (d.z == d.w) qs_next = qscale(ex);
           else Xw[size_t(d.z) * 32] = ex;

@@ -222,8 +222,12 @@ def test_walk4s_table_width_and_kernel_agree(monkeypatch):
         assert_vec(rep.branch_gradient, g)
         assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
     a, b = reps["nc4"], reps["nc5"]
-    # the extra zero column changes nothing but the table layout
-    assert a.log_likelihood == b.log_likelihood and np.array_equal(a.branch_gradient, b.branch_gradient)
+    # the post-order pass is the same arithmetic (the cherry tables of the
+    # 4-column kernel are exact); the fused cherry steps of its pre-order pass
+    # share the parent's denominator, so the gradients agree to rounding
+    assert a.log_likelihood == b.log_likelihood
+    np.testing.assert_allclose(a.branch_gradient, b.branch_gradient, rtol=1e-12,
+                               atol=1e-14 * np.abs(b.branch_gradient).max())
     np.testing.assert_allclose(reps["walk4"].branch_gradient, a.branch_gradient, rtol=1e-12,
                                atol=1e-14 * np.abs(a.branch_gradient).max())
 
