@@ -32,7 +32,9 @@ void* pg_walk4t_kernel(bool hess, int nc);
 size_t pg_walk4t_smem(int nc);
 size_t pg_walk4s_smem(int nc);
 void* pg_walk4s_cherry_kernel(bool homog, bool hess);
-void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, double* ct, cudaStream_t stream);
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, const double* qtc, double* ct,
+                      cudaStream_t stream);
+size_t pg_walk4s_cherry_smem();
 void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,
                      cudaStream_t stream);
 static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
@@ -121,6 +123,12 @@ struct pg_engine {
   // walk4s cherry tables (pg_walk4s.cuh): {k, a, b, 0} per cherry, the step
   // lists with the children's cherry flags (post: without the cherries' steps)
   bool use_cherry = false;
+  // gapless 4-state data through walk4s on a tree with a cherry (any binary tree
+  // of more than two tips); PG_WALK4S_CHERRY=0 turns the tables off, for A/B
+  bool cherry_wanted() const {
+    return use_walk4 && use_walk4s && NC == 4 && m == 4 && N > 2 &&
+           !(std::getenv("PG_WALK4S_CHERRY") && std::atoi(std::getenv("PG_WALK4S_CHERRY")) == 0);
+  }
   std::vector<int4> cherries, post_steps_ch, pre_steps_ch, pre_steps_fused;
   // patterns
   int m_aln = 0, P = 0, A = 0;
@@ -665,6 +673,7 @@ struct pg_engine {
       walk_smem = use_walk4t   ? pg_walk4t_smem(NC)
                   : use_walk4s ? pg_walk4s_smem(NC)
                              : size_t(pgk::kWarpsPerBlock) * 2 * pgk::walk4_stage_d2(walk4_lcv, L, NC) * sizeof(double2);
+      if (cherry_wanted()) walk_smem = std::max(walk_smem, pg_walk4s_cherry_smem());
     }
     if (use_walkl) {
       G = L;
@@ -747,8 +756,7 @@ struct pg_engine {
     // (PG_WALK4S_CHERRY=0 turns them off, for A/B)
     use_cherry = false;
     cherries.clear();
-    if (use_walk4 && use_walk4s && NC == 4 && m == 4 && N > 2 &&
-        !(std::getenv("PG_WALK4S_CHERRY") && std::atoi(std::getenv("PG_WALK4S_CHERRY")) == 0)) {
+    if (cherry_wanted()) {
       std::vector<char> is_ch(size_t(2 * N), 0);
       for (const int4& st : post_steps)
         if (st.x != 2 * N - 1 && st.y <= N && st.z <= N) {
@@ -859,7 +867,7 @@ struct pg_engine {
       launch_tc();
       ++launches;
       if (use_cherry) {
-        pg_cherry_tables(d_cherries.p, int(cherries.size()), N, d_tc.p, d_ct.p, stream);
+        pg_cherry_tables(d_cherries.p, int(cherries.size()), N, d_tc.p, d_qtc.p, d_ct.p, stream);
         PG_CUDA(cudaGetLastError());
         ++launches;
       }
@@ -1043,8 +1051,8 @@ int pg_engine::walk_max_blocks_per_sm_occ() {
       int b = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, pgk::kWarpsPerBlock * 32, walk_smem));
       nb = v == 0 ? b : std::min(nb, b);
-      if (use_walk4s && NC == 4) {
-        // the cherry-table instances share the grid (decided before the cherries are known)
+      if (cherry_wanted()) {
+        // the cherry-table instances (3 CTAs per SM) set the grid
         const void* fc = pg_walk4s_cherry_kernel(branch_q.empty(), v & 1);
         PG_CUDA(cudaFuncSetAttribute(fc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fc, pgk::kWarpsPerBlock * 32, walk_smem));
@@ -1199,7 +1207,8 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       ps.ct = use_cherry ? d_ct.p : nullptr;
       ps.ccodes = use_cherry ? d_ccodes.p : nullptr;
       ps.npost = use_cherry ? int(post_steps_ch.size()) : int(post_steps.size());
-      if (use_cherry && branch_q.empty()) ps.w.p.pre = d_pre_fused.p;  // fused cherry steps (HOMOG instances)
+      // fused cherry steps: the gradient instances (W tables) and the one-generator Hessian ones
+      if (use_cherry && (!do_hess || branch_q.empty())) ps.w.p.pre = d_pre_fused.p;
       void* fn = use_cherry ? pg_walk4s_cherry_kernel(branch_q.empty(), do_hess)
                             : pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
       void* args[] = {&ps};

@@ -121,7 +121,9 @@ struct Walk4Params {
 
 // cherry flags of a step's children in its descriptor's x (pg_walk4s.cuh, CH instances)
 constexpr int kCherryY = 1 << 29, kCherryZ = 1 << 30, kNodeMask = kCherryY - 1;
-constexpr int kCherryBlk = 200;  // double2 per cherry block: e_k table (128) | TC_u (32) | TC_v (32) | tip ids (1) | pad
+// double2 per cherry block: e_k table [0,128) | TC_u [128,160) | TC_v [160,192) | tip ids [192] | pad |
+// W_u [200,328) | W_v [328,456)
+constexpr int kCherryBlk = 456;
 
 // Parameters of the single-buffered 4-state kernel (pg_walk4s.cuh).
 struct Walk4SParams {

@@ -17,8 +17,15 @@ void* pg_walk4s_cherry_kernel(bool homog, bool hess) {
               : reinterpret_cast<void*>(&pgk::walk4s_kernel<false, false, 4, true>);
 }
 
-void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, double* ct, cudaStream_t stream) {
-  if (ncherry > 0) pgk::cherry_tc_kernel<<<(ncherry * 64 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, ct);
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, const double* qtc, double* ct,
+                      cudaStream_t stream) {
+  if (ncherry > 0)
+    pgk::cherry_tc_kernel<<<(ncherry * 64 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, qtc, ct);
+}
+
+// dynamic shared memory of the cherry instances (the gradient ones hold three tables per cherry child)
+size_t pg_walk4s_cherry_smem() {
+  return size_t(pgk::kWarpsPerBlock) * pgk::Walk4SGeom<4, true>::WARP * sizeof(double2);
 }
 
 void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,

@@ -52,16 +52,18 @@
 
 namespace pgk {
 
-template <int NC>
+// WT: slots A and B also hold a cherry child's three tables + tip ids (below)
+template <int NC, bool WT = false>
 struct Walk4SGeom {
   static constexpr int MP = 4, L = 4;
   static constexpr int TCB = L * NC * MP;  // doubles per node TC block
   static constexpr int TCC = TCB / 2;      // double2 chunks per TC block
   static constexpr int VEC = 32 * L * MP;  // doubles per node slot of one warp
   static constexpr int SD2 = VEC / 2;      // double2 per node slot
+  static constexpr int SDA = WT ? 392 : SD2;  // double2 per slot A / B (WT: 3 x 128 + ids, 128-byte multiple)
   // per warp: slots Q, A, B; TC blocks 0, 1; exponent row (32 ints)
   // (rounded up to 128 bytes: a 64-byte offset makes every 512-byte slot access 5 wavefronts)
-  static constexpr int WARP = (3 * SD2 + 2 * TCC + 8 + 7) & ~7;  // double2
+  static constexpr int WARP = (SD2 + 2 * SDA + 2 * TCC + 8 + 7) & ~7;  // double2
 };
 
 // Cherry tables (CH instances; NC = 4, no missing / ambiguous tip codes): the
@@ -75,17 +77,25 @@ struct Walk4SGeom {
 // table into a free operand slot and gathers.  The table is left unnormalised
 // (the parent's own power-of-two normalisation absorbs the scale exactly).
 // Step descriptors carry the children's cherry flags in bits 29 / 30 of x.
-// With one shared generator (HOMOG) the cherry's pre-order step is fused into
-// its parent's as well: q_k = P_k^T top stays in registers and the two tips'
-// gradient terms are formed on the spot from their TC blocks (staged behind
-// the table: a cherry block is [e_k table 2 KB | TC_u | TC_v | tip node ids],
-// kCherryBlk double2), against the parent's own denominator (Eq. 8: q_k . (e_u
-// o e_v) = top_k . e_k) -- no hand-off or scratch round trip of q_k, no
-// normalisation, a third fewer pre-order steps.
+// The cherry's pre-order step (the gradients of its tips u, v) is fused into
+// its parent's, against the parent's own denominator (Eq. 8: q_k . (e_u o e_v)
+// = top_k . e_k), so a third of the pre-order steps and every hand-off or
+// scratch round trip of q_k go away too:
+//  * gradient instances (WT): the tips' numerators q_k . (e_v o Q e_u) with
+//    q_k = P_k^T top_k are top_k . W_u for the tabulated W_u = P_k (e_v o Q e_u)
+//    (and W_v alike; Q e of a tip from K1's Q P columns, so per-branch
+//    generators are covered): two more gathers and 8 FMAs per category, no
+//    P_k^T mat-vec, no P_k^T block; slots A / B grow to 6.1 KB for the three
+//    tables (12 warps per SM);
+//  * Hessian instances with one shared generator: q_k = P_k^T top_k stays in
+//    registers and the tips' terms are formed from their TC blocks (behind the
+//    table in the cherry block); with per-branch generators the cherry keeps
+//    its own step.
+// A cherry block (kCherryBlk double2) is [e_k | TC_u | TC_v | ids | W_u | W_v].
 
 // one thread per (cherry, category, code pair); TC is [B][4][4][4]
 static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int ncherry, int N, const double* __restrict__ tc,
-                                 double* __restrict__ ct) {
+                                        const double* __restrict__ qtc, double* __restrict__ ct) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncherry * 64) return;
   const int ci = i >> 6, l = (i >> 4) & 3, combo = i & 15;
@@ -93,17 +103,28 @@ static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int n
   const double* Ta = tc + (size_t(ch.y - 1) * 4 + l) * 16 + (combo >> 2) * 4;
   const double* Tb = tc + (size_t(ch.z - 1) * 4 + l) * 16 + (combo & 3) * 4;
   const double* Tk = tc + (size_t(ch.x - 1) * 4 + l) * 16;
-  double e[4] = {0.0, 0.0, 0.0, 0.0};
+  // Q e of the tips (K1's Q P columns, same layout as TC)
+  const double* Qa = qtc + (Ta - tc);
+  const double* Qb = qtc + (Tb - tc);
+  double e[4] = {0.0, 0.0, 0.0, 0.0}, wu[4] = {0.0, 0.0, 0.0, 0.0}, wv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const double xc = Ta[c] * Tb[c];
+    const double xc = Ta[c] * Tb[c], xu = Tb[c] * Qa[c], xv = Ta[c] * Qb[c];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) e[r] = fma(Tk[c * 4 + r], xc, e[r]);
+    for (int r = 0; r < 4; ++r) {
+      e[r] = fma(Tk[c * 4 + r], xc, e[r]);
+      wu[r] = fma(Tk[c * 4 + r], xu, wu[r]);
+      wv[r] = fma(Tk[c * 4 + r], xv, wv[r]);
+    }
   }
   double* blk = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk);
   double* out = blk + l * 64 + combo * 4;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) out[r] = e[r];
+  for (int r = 0; r < 4; ++r) {
+    out[r] = e[r];
+    out[2 * 200 + r] = wu[r];
+    out[2 * 328 + r] = wv[r];
+  }
   // the tips' own TC blocks (32 double2 each) and node ids behind the table
   const int t64 = i & 63;
   const double2* src = reinterpret_cast<const double2*>(tc + size_t((t64 < 32 ? ch.y : ch.z) - 1) * 64) + (t64 & 31);
@@ -126,8 +147,11 @@ template <bool HOMOG, bool HESS, int NC, bool CH = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : PG_WALK4S_MINB)
     walk4s_kernel(const __grid_constant__ Walk4SParams PS) {
   static_assert(!CH || NC == 4, "cherry tables: 4 x 4 code pairs");
-  using Gm = Walk4SGeom<NC>;
-  constexpr int L = 4, TCC = Gm::TCC, VEC = Gm::VEC, SD2 = Gm::SD2;
+  constexpr bool WT = CH && !HESS;               // fused cherry steps through the W tables
+  constexpr bool FUSE_TC = CH && HESS && HOMOG;  // fused through the tips' TC blocks
+  constexpr bool FUSE = WT || FUSE_TC;
+  using Gm = Walk4SGeom<NC, WT>;
+  constexpr int L = 4, TCC = Gm::TCC, VEC = Gm::VEC, SD2 = Gm::SD2, SDA = Gm::SDA;
   static_assert(TCC <= SD2, "a TC block fits in an operand slot");
   const Walk4Params& P4 = PS.w;
   const WalkParams& p = P4.p;
@@ -140,8 +164,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
   double2* const wsm = reinterpret_cast<double2*>(smem_raw) + size_t(wib) * Gm::WARP;
   double2* const sQ = wsm;
   double2* const sA = wsm + SD2;
-  double2* const sB = wsm + 2 * SD2;
-  double2* const sT0 = wsm + 3 * SD2;
+  double2* const sB = sA + SDA;
+  double2* const sT0 = sB + SDA;
   double2* const sT1 = sT0 + TCC;
   double2* const sX = sT1 + TCC;  // exponent row of a staged pre-partial
 
@@ -211,7 +235,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
     for (int c = 0; c < 6; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
     if (lane == 0) cp16_ca(d + 192, gs + 192);
   };
-  constexpr bool FUSE = CH && HOMOG;
+  // (WT) e_k, W_u, W_v and the ids: slot [0,128) [128,256) [256,384) [384]
+  auto stage_cw = [&](double2* d, int node) {
+    const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cp16_ca(d + 128 + c * 32 + lane, gs + 200 + c * 32);
+    if (lane == 0) cp16_ca(d + 384, gs + 192);
+  };
+  constexpr int kIdsAt = WT ? 384 : 192;
   // descriptor -> node ids + the children's cherry flags (bit 0: y, bit 1: z)
   auto unflag = [&](int4& d) -> int {
     if constexpr (!CH) return 0;
@@ -424,7 +457,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
           cn0 = code_ld(d.y);
         } else if (CH && (f & 1)) {
           cn0 = ccode_ld(d.y);
-          if constexpr (FUSE) stage_cb(sA, d.y);
+          if constexpr (WT) stage_cw(sA, d.y);
+          else if constexpr (FUSE_TC) stage_cb(sA, d.y);
           else stage_ct(sA, d.y);
         } else {
           stage_slot_once(sA, Eb + size_t(d.y) * SD2);
@@ -433,13 +467,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
           cn1 = code_ld(d.z);
         } else if (CH && (f & 2)) {
           cn1 = ccode_ld(d.z);
-          if constexpr (FUSE) stage_cb(sB, d.z);
+          if constexpr (WT) stage_cw(sB, d.z);
+          else if constexpr (FUSE_TC) stage_cb(sB, d.z);
           else stage_ct(sB, d.z);
         } else {
           stage_slot_once(sB, Eb + size_t(d.z) * SD2);
         }
-        stage_blk(sT0, p.tc, d.y);
-        stage_blk(sT1, p.tc, d.z);
+        // (WT) a cherry child needs no P^T block
+        if (!(WT && (f & 1))) stage_blk(sT0, p.tc, d.y);
+        if (!(WT && (f & 2))) stage_blk(sT1, p.tc, d.z);
       };
       const char* base_e = reinterpret_cast<const char*>(p.escr + wbase * VEC);
       const int n = FUSE ? PS.npost : p.nsteps;  // (FUSE) the cherries' own steps are gone
@@ -596,7 +632,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
           // outgoing pre-partials q_x = P_x^T top (engine.hpp:249-250),
           // unnormalised: the child visited next in place into slot Q (this
           // category's q was read above), the other to its scratch slot
-          if (a_int) {
+          if (WT && a_ch) {
+            double wu[4], wv[4];
+            gather_ct(sA + 128, code0, j, wu);
+            gather_ct(sA + 256, code0, j, wv);
+            double du = 0.0, dv = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              du = fma(ta[r], wu[r], du);
+              dv = fma(ta[r], wv[r], dv);
+            }
+            cau = fma(PS.crw[j], du, cau);
+            cav = fma(PS.crw[j], dv, cav);
+          } else if (a_int) {
             const double2* Tl = sT0 + j * NC * 2;
             double o[4];
 #pragma unroll
@@ -605,14 +653,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
               o[c] = fma(u.x, ta[0], fma(u.y, ta[1], fma(v.x, ta[2], v.y * ta[3])));
               ha = max(ha, __double2hiint(o[c]));
             }
-            if (a_fuse) fused_tips(sA, code0, j, o, cau, cav, cau2, cav2);
+            if (FUSE_TC && a_ch) fused_tips(sA, code0, j, o, cau, cav, cau2, cav2);
             else if (d.y == d.w) write_cat(sQ, j, o);
             else {
               __stcg(qa_dst + (2 * j) * 32, make_double2(o[0], o[1]));
               __stcg(qa_dst + (2 * j + 1) * 32, make_double2(o[2], o[3]));
             }
           }
-          if (b_int) {
+          if (WT && b_ch) {
+            double wu[4], wv[4];
+            gather_ct(sB + 128, code1, j, wu);
+            gather_ct(sB + 256, code1, j, wv);
+            double du = 0.0, dv = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              du = fma(tb[r], wu[r], du);
+              dv = fma(tb[r], wv[r], dv);
+            }
+            cbu = fma(PS.crw[j], du, cbu);
+            cbv = fma(PS.crw[j], dv, cbv);
+          } else if (b_int) {
             const double2* Tl = sT1 + j * NC * 2;
             double o[4];
 #pragma unroll
@@ -621,7 +681,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
               o[c] = fma(u.x, tb[0], fma(u.y, tb[1], fma(v.x, tb[2], v.y * tb[3])));
               hb = max(hb, __double2hiint(o[c]));
             }
-            if (b_fuse) fused_tips(sB, code1, j, o, cbu, cbv, cbu2, cbv2);
+            if (FUSE_TC && b_ch) fused_tips(sB, code1, j, o, cbu, cbv, cbu2, cbv2);
             else if (d.z == d.w) write_cat(sQ, j, o);
             else {
               __stcg(qb_dst + (2 * j) * 32, make_double2(o[0], o[1]));
@@ -631,8 +691,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
         }
         // (FUSE) the fused tips' node ids (lane 0: u, lane 16: v) before the slots are refilled
         int ida = 0, idb = 0;
-        if (a_fuse) ida = reinterpret_cast<const int*>(sA + 192)[lane >> 4];
-        if (b_fuse) idb = reinterpret_cast<const int*>(sB + 192)[lane >> 4];
+        if (a_fuse) ida = reinterpret_cast<const int*>(sA + kIdsAt)[lane >> 4];
+        if (b_fuse) idb = reinterpret_cast<const int*>(sB + kIdsAt)[lane >> 4];
         __syncwarp();
         // the next step's operands (slots A, B, TC blocks; slot Q
         // unless its pre-partial was just handed on there)
