@@ -294,8 +294,9 @@ def _caterpillar_newick(tips, rng):
 @pytest.mark.parametrize("branch_q", [False, True], ids=["homog", "per_branch_q"])
 def test_walk4s_cherry_tables(shape, branch_q, monkeypatch):
     """walk4s with cherry tables (a node with two tip children tabulated per
-    code pair, pg_walk4s.cuh CH instances) against the oracle and against the
-    same kernel without them, with the Hessian: a balanced tree (every tip in a
+    code pair, its pre-order step fused into its parent's; pg_walk4s.cuh CH
+    instances) against the oracle and against the same kernel without them,
+    gradient only and with the Hessian: a balanced tree (every tip in a
     cherry, parents of two cherries), a caterpillar (one cherry at the
     bottom), a small tree with a cherry directly under the root and a random
     Yule tree."""
@@ -314,22 +315,28 @@ def test_walk4s_cherry_tables(shape, branch_q, monkeypatch):
     monkeypatch.setenv("PG_WALKL", "0")
     monkeypatch.setenv("PG_WALK4_LCV", "4")
     monkeypatch.setenv("PG_WALK4S", "1")
-    reps = {}
+    reps, grads = {}, {}
     for ch in ("1", "0"):
         monkeypatch.setenv("PG_WALK4S_CHERRY", ch)
         if nw is None:
             eng, ref = _instance_pair(inst, _branch_q(3, inst.branches) if branch_q else ())
         else:
             eng, ref = _newick_pair(nw, 30000, 17, branch_q=branch_q)
-        reps[ch] = eng.branch_gradient(True)
-        assert eng.info()["kernel"] == "walk4s_kernel"
+        # gradient only (cherry steps fused through the W tables) and with the
+        # Hessian (fused through the tips' TC blocks, or unfused per-branch)
+        grads[ch] = eng.branch_gradient(False)
         # K1 + cherry tables + walk + reduce with the tables, K1 + walk + reduce without
         assert eng.info()["launches"] == (4 if ch == "1" else 3)
+        reps[ch] = eng.branch_gradient(True)
+        assert eng.info()["kernel"] == "walk4s_kernel"
     ll, g, h = ref.branch_gradient(True)
     for rep in reps.values():
         assert_logl(rep.log_likelihood, ll)
         assert_vec(rep.branch_gradient, g)
         assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    for rep in grads.values():
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(rep.branch_gradient, g)
     a, b = reps["1"], reps["0"]
     np.testing.assert_allclose(a.log_likelihood, b.log_likelihood, rtol=1e-14)
     np.testing.assert_allclose(a.branch_gradient, b.branch_gradient, rtol=1e-11,
