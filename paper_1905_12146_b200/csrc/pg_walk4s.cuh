@@ -52,6 +52,20 @@
 
 namespace pgk {
 
+// table copies (TC blocks, cherry blocks): .cg by default -- with the shared
+// memory carve-out this kernel needs, almost no L1 is left to allocate into
+// (C3 100.1 / 101.8 ms vs 103.0 / 103.7 ms with .ca on one box)
+#ifndef PG_W4S_TABLE_CG
+#define PG_W4S_TABLE_CG 1
+#endif
+__device__ __forceinline__ void cp16_tab(void* smem, const void* gmem) {
+#if PG_W4S_TABLE_CG
+  cp16_cg(smem, gmem);
+#else
+  cp16_ca(smem, gmem);
+#endif
+}
+
 // WT: slots A and B also hold a cherry child's three tables + tip ids (below)
 template <int NC, bool WT = false>
 struct Walk4SGeom {
@@ -192,7 +206,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
     const double2* gs = reinterpret_cast<const double2*>(table) + size_t(node - 1) * TCC;
 #pragma unroll
     for (int c = 0; c < (TCC + 31) / 32; ++c)
-      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
+      if (c * 32 + lane < TCC) cp16_tab(d + c * 32 + lane, gs + c * 32 + lane);
   };
   const size_t Pc = size_t(p.Pc);
   auto read_cat = [&](const double2* slot, int j, double (&v)[4]) {
@@ -226,23 +240,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
   auto stage_ct = [&](double2* d, int node) {
     const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
+    for (int c = 0; c < 4; ++c) cp16_tab(d + c * 32 + lane, gs + c * 32);
   };
   // the whole cherry block (table, the tips' TC blocks, their node ids)
   auto stage_cb = [&](double2* d, int node) {
     const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
 #pragma unroll
-    for (int c = 0; c < 6; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
-    if (lane == 0) cp16_ca(d + 192, gs + 192);
+    for (int c = 0; c < 6; ++c) cp16_tab(d + c * 32 + lane, gs + c * 32);
+    if (lane == 0) cp16_tab(d + 192, gs + 192);
   };
   // (WT) e_k, W_u, W_v and the ids: slot [0,128) [128,256) [256,384) [384]
   auto stage_cw = [&](double2* d, int node) {
     const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp16_ca(d + c * 32 + lane, gs + c * 32);
+    for (int c = 0; c < 4; ++c) cp16_tab(d + c * 32 + lane, gs + c * 32);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) cp16_ca(d + 128 + c * 32 + lane, gs + 200 + c * 32);
-    if (lane == 0) cp16_ca(d + 384, gs + 192);
+    for (int c = 0; c < 8; ++c) cp16_tab(d + 128 + c * 32 + lane, gs + 200 + c * 32);
+    if (lane == 0) cp16_tab(d + 384, gs + 192);
   };
   constexpr int kIdsAt = WT ? 384 : 192;
   // descriptor -> node ids + the children's cherry flags (bit 0: y, bit 1: z)
