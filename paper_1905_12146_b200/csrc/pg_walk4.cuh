@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   };
   // the tile's TP code bytes of one tip (16 B chunks)
   auto stage_codes = [&](int stage, int which, const uint8_t* row) {
-    if (lane < TP / 16) cp16_ca(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2 + lane, row + 16 * lane);
+    if (lane < TP / 16) cp16_cg(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2 + lane, row + 16 * lane);
   };
   auto code_of = [&](int stage, int which) -> int {
     return reinterpret_cast<const uint8_t*>(wsm + stage * STAGE + 3 * SD2 + 3 * TCC + which * 2)[pl];
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
     double2* d = wsm + stage * STAGE + slot * SD2;
 #pragma unroll
     for (int c = 0; c < (TCC + 31) / 32; ++c)
-      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
+      if (c * 32 + lane < TCC) cp16_cg(d + c * 32 + lane, gs + c * 32 + lane);
   };
   auto qtp = [&](int stage, int slot) -> const double* {
     return reinterpret_cast<const double*>(wsm + stage * STAGE + slot * SD2);
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
     double2* d = wsm + stage * STAGE + 3 * SD2 + slot * TCC;
 #pragma unroll
     for (int c = 0; c < (TCC + 31) / 32; ++c)
-      if (c * 32 + lane < TCC) cp16_ca(d + c * 32 + lane, gs + c * 32 + lane);
+      if (c * 32 + lane < TCC) cp16_cg(d + c * 32 + lane, gs + c * 32 + lane);
   };
   // one category (4 doubles) of a lane's slot: double2 q = 2j, 2j+1
   auto read_cat = [&](const double2* src, int j, double (&v)[4]) {
