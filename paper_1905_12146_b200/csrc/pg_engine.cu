@@ -31,11 +31,11 @@ void* pg_walk4s_kernel(bool homog, bool hess, int nc);
 void* pg_walk4t_kernel(bool hess, int nc);
 size_t pg_walk4t_smem(int nc);
 size_t pg_walk4s_smem(int nc);
-void* pg_walk4s_cherry_kernel(bool homog, bool hess);
-void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, const double* qtc, double* ct,
+void* pg_walk4s_cherry_kernel(bool homog, bool hess, int nc);
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, int nc, const double* tc, const double* qtc, double* ct,
                       cudaStream_t stream);
 size_t pg_walk4s_cherry_smem();
-void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,
+void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, int nc, const uint8_t* codes, uint8_t* cc,
                      cudaStream_t stream);
 static void* pg_walk4_kernel(bool homog, bool hess, int nc, int lcv, int L) {
   if (L != 4) return pg_walk4_kernel_l12(homog, hess, nc, L);
@@ -123,10 +123,11 @@ struct pg_engine {
   // walk4s cherry tables (pg_walk4s.cuh): {k, a, b, 0} per cherry, the step
   // lists with the children's cherry flags (post: without the cherries' steps)
   bool use_cherry = false;
-  // gapless 4-state data through walk4s on a tree with a cherry (any binary tree
-  // of more than two tips); PG_WALK4S_CHERRY=0 turns the tables off, for A/B
+  // 4-state data without ambiguity classes (NC = 4; with missing characters
+  // NC = 5) through walk4s on a tree with a cherry (any binary tree of more
+  // than two tips); PG_WALK4S_CHERRY=0 turns the tables off, for A/B
   bool cherry_wanted() const {
-    return use_walk4 && use_walk4s && NC == 4 && m == 4 && N > 2 &&
+    return use_walk4 && use_walk4s && (NC == 4 || (NC == 5 && A == 1)) && m == 4 && N > 2 &&
            !(std::getenv("PG_WALK4S_CHERRY") && std::atoi(std::getenv("PG_WALK4S_CHERRY")) == 0);
   }
   std::vector<int4> cherries, post_steps_ch, pre_steps_ch, pre_steps_fused;
@@ -673,7 +674,7 @@ struct pg_engine {
       walk_smem = use_walk4t   ? pg_walk4t_smem(NC)
                   : use_walk4s ? pg_walk4s_smem(NC)
                              : size_t(pgk::kWarpsPerBlock) * 2 * pgk::walk4_stage_d2(walk4_lcv, L, NC) * sizeof(double2);
-      if (cherry_wanted()) walk_smem = std::max(walk_smem, pg_walk4s_cherry_smem());
+      if (cherry_wanted() && NC == 4) walk_smem = std::max(walk_smem, pg_walk4s_cherry_smem());
     }
     if (use_walkl) {
       G = L;
@@ -791,7 +792,7 @@ struct pg_engine {
         d_cherries.upload(cherries.data(), cherries.size(), stream);
         d_ct.ensure(size_t(N - 1) * 2 * pgk::kCherryBlk);
         d_ccodes.ensure(size_t(N - 1) * size_t(Pc));
-        pg_cherry_codes(d_cherries.p, int(cherries.size()), N, Pc, d_codes.p, d_ccodes.p, stream);
+        pg_cherry_codes(d_cherries.p, int(cherries.size()), N, Pc, NC, d_codes.p, d_ccodes.p, stream);
         PG_CUDA(cudaGetLastError());
       }
     }
@@ -867,7 +868,7 @@ struct pg_engine {
       launch_tc();
       ++launches;
       if (use_cherry) {
-        pg_cherry_tables(d_cherries.p, int(cherries.size()), N, d_tc.p, d_qtc.p, d_ct.p, stream);
+        pg_cherry_tables(d_cherries.p, int(cherries.size()), N, NC, d_tc.p, d_qtc.p, d_ct.p, stream);
         PG_CUDA(cudaGetLastError());
         ++launches;
       }
@@ -1053,7 +1054,7 @@ int pg_engine::walk_max_blocks_per_sm_occ() {
       nb = v == 0 ? b : std::min(nb, b);
       if (cherry_wanted()) {
         // the cherry-table instances (3 CTAs per SM) set the grid
-        const void* fc = pg_walk4s_cherry_kernel(branch_q.empty(), v & 1);
+        const void* fc = pg_walk4s_cherry_kernel(branch_q.empty(), v & 1, NC);
         PG_CUDA(cudaFuncSetAttribute(fc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem)));
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fc, pgk::kWarpsPerBlock * 32, walk_smem));
         nb = std::min(nb, b);
@@ -1208,8 +1209,8 @@ void pg_engine::launch_walk(bool do_pre, bool do_hess) {
       ps.ccodes = use_cherry ? d_ccodes.p : nullptr;
       ps.npost = use_cherry ? int(post_steps_ch.size()) : int(post_steps.size());
       // fused cherry steps: the gradient instances (W tables) and the one-generator Hessian ones
-      if (use_cherry && (!do_hess || branch_q.empty())) ps.w.p.pre = d_pre_fused.p;
-      void* fn = use_cherry ? pg_walk4s_cherry_kernel(branch_q.empty(), do_hess)
+      if (use_cherry && NC == 4 && (!do_hess || branch_q.empty())) ps.w.p.pre = d_pre_fused.p;
+      void* fn = use_cherry ? pg_walk4s_cherry_kernel(branch_q.empty(), do_hess, NC)
                             : pg_walk4s_kernel(branch_q.empty(), do_hess, NC);
       void* args[] = {&ps};
       PG_CUDA(cudaLaunchKernel(fn, dim3(unsigned(TW / pgk::kWarpsPerBlock)), dim3(pgk::kWarpsPerBlock * 32), args,

@@ -9,18 +9,23 @@
 #define PG_W4S(H, S, NC) \
   if (homog == H && hess == S && nc == NC) return reinterpret_cast<void*>(&pgk::walk4s_kernel<H, S, NC>);
 
-// cherry-table instances (NC = 4)
-void* pg_walk4s_cherry_kernel(bool homog, bool hess) {
-  if (homog) return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<true, true, 4, true>)
-                         : reinterpret_cast<void*>(&pgk::walk4s_kernel<true, false, 4, true>);
-  return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<false, true, 4, true>)
-              : reinterpret_cast<void*>(&pgk::walk4s_kernel<false, false, 4, true>);
+// cherry-table instances (NC = 4: fused cherry steps; NC = 5: the e_k tables alone)
+template <int NC>
+static void* cherry_pick(bool homog, bool hess) {
+  if (homog) return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<true, true, NC, true>)
+                         : reinterpret_cast<void*>(&pgk::walk4s_kernel<true, false, NC, true>);
+  return hess ? reinterpret_cast<void*>(&pgk::walk4s_kernel<false, true, NC, true>)
+              : reinterpret_cast<void*>(&pgk::walk4s_kernel<false, false, NC, true>);
+}
+void* pg_walk4s_cherry_kernel(bool homog, bool hess, int nc) {
+  return nc == 4 ? cherry_pick<4>(homog, hess) : nc == 5 ? cherry_pick<5>(homog, hess) : nullptr;
 }
 
-void pg_cherry_tables(const int4* cherries, int ncherry, int N, const double* tc, const double* qtc, double* ct,
+void pg_cherry_tables(const int4* cherries, int ncherry, int N, int nc, const double* tc, const double* qtc, double* ct,
                       cudaStream_t stream) {
-  if (ncherry > 0)
-    pgk::cherry_tc_kernel<<<(ncherry * 64 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, qtc, ct);
+  if (ncherry <= 0) return;
+  if (nc == 4) pgk::cherry_tc_kernel<<<(ncherry * 64 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, qtc, ct);
+  else pgk::cherry_tc5_kernel<<<(ncherry * 100 + 127) / 128, 128, 0, stream>>>(cherries, ncherry, N, tc, ct);
 }
 
 // dynamic shared memory of the cherry instances (the gradient ones hold three tables per cherry child)
@@ -28,11 +33,11 @@ size_t pg_walk4s_cherry_smem() {
   return size_t(pgk::kWarpsPerBlock) * pgk::Walk4SGeom<4, true>::WARP * sizeof(double2);
 }
 
-void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, const uint8_t* codes, uint8_t* cc,
+void pg_cherry_codes(const int4* cherries, int ncherry, int N, long long Pc, int nc, const uint8_t* codes, uint8_t* cc,
                      cudaStream_t stream) {
   if (ncherry <= 0) return;
   const unsigned gx = unsigned(std::min<long long>((Pc + 255) / 256, 64));
-  pgk::cherry_codes_kernel<<<dim3(gx, unsigned(ncherry)), 256, 0, stream>>>(cherries, ncherry, N, Pc, codes, cc);
+  pgk::cherry_codes_kernel<<<dim3(gx, unsigned(ncherry)), 256, 0, stream>>>(cherries, ncherry, N, Pc, nc, codes, cc);
 }
 
 void* pg_walk4s_kernel(bool homog, bool hess, int nc) {

@@ -146,23 +146,50 @@ static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int n
   if (t64 == 0) *reinterpret_cast<int4*>(blk + 2 * 192) = make_int4(ch.y, ch.z, 0, 0);
 }
 
-// combined code rows of the cherries: cc[k - N - 1][s] = 4 code_a[s] + code_b[s]
-static __global__ void cherry_codes_kernel(const int4* __restrict__ cherries, int ncherry, int N, long long Pc,
+// Data with missing characters (NC = 5: the four states + the all-ones column):
+// the e_k table alone, 25 code pairs (3.2 KB, it fits the 4 KB operand slots);
+// the cherry keeps its own pre-order step.  One thread per (cherry, category,
+// code pair); TC is [B][4][5][4].
+static __global__ void cherry_tc5_kernel(const int4* __restrict__ cherries, int ncherry, int N,
+                                         const double* __restrict__ tc, double* __restrict__ ct) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncherry * 100) return;
+  const int ci = i / 100, l = (i % 100) / 25, combo = i % 25;
+  const int4 ch = cherries[ci];
+  const double* Ta = tc + (size_t(ch.y - 1) * 4 + l) * 20 + (combo / 5) * 4;
+  const double* Tb = tc + (size_t(ch.z - 1) * 4 + l) * 20 + (combo % 5) * 4;
+  const double* Tk = tc + (size_t(ch.x - 1) * 4 + l) * 20;
+  double e[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double xc = Ta[c] * Tb[c];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) e[r] = fma(Tk[c * 4 + r], xc, e[r]);
+  }
+  double* out = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk) + l * 100 + combo * 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) out[r] = e[r];
+}
+
+// combined code rows of the cherries: cc[k - N - 1][s] = nc code_a[s] + code_b[s]
+static __global__ void cherry_codes_kernel(const int4* __restrict__ cherries, int ncherry, int N, long long Pc, int nc,
                                     const uint8_t* __restrict__ codes, uint8_t* __restrict__ cc) {
   const int4 ch = cherries[blockIdx.y];
   const uint8_t* a = codes + size_t(ch.y - 1) * Pc;
   const uint8_t* b = codes + size_t(ch.z - 1) * Pc;
   uint8_t* o = cc + size_t(ch.x - N - 1) * Pc;
   for (long long s = blockIdx.x * blockDim.x + threadIdx.x; s < Pc; s += (long long)gridDim.x * blockDim.x)
-    o[s] = uint8_t(4 * (a[s] & 3) + (b[s] & 3));
+    o[s] = uint8_t(nc * min(int(a[s]), nc - 1) + min(int(b[s]), nc - 1));
 }
 
 template <bool HOMOG, bool HESS, int NC, bool CH = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : PG_WALK4S_MINB)
     walk4s_kernel(const __grid_constant__ Walk4SParams PS) {
-  static_assert(!CH || NC == 4, "cherry tables: 4 x 4 code pairs");
-  constexpr bool WT = CH && !HESS;               // fused cherry steps through the W tables
-  constexpr bool FUSE_TC = CH && HESS && HOMOG;  // fused through the tips' TC blocks
+  static_assert(!CH || NC == 4 || NC == 5, "cherry tables: 4 x 4 or 5 x 5 code pairs");
+  constexpr bool WT = CH && !HESS && NC == 4;               // fused cherry steps through the W tables
+  constexpr bool FUSE_TC = CH && HESS && HOMOG && NC == 4;  // fused through the tips' TC blocks
+  constexpr int NCC = NC * NC;         // code pairs of a cherry
+  constexpr int TBLC = 4 * NCC * 2;    // double2 per e_k table
   constexpr bool FUSE = WT || FUSE_TC;
   using Gm = Walk4SGeom<NC, WT>;
   constexpr int L = 4, TCC = Gm::TCC, VEC = Gm::VEC, SD2 = Gm::SD2, SDA = Gm::SDA;
@@ -230,7 +257,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
   };
   // a cherry's table [category][code pair][4] staged in an operand slot
   auto gather_ct = [&](const double2* tbl, int code, int j, double (&v)[4]) {
-    const double2* c = tbl + (j * 16 + code) * 2;
+    const double2* c = tbl + (j * NCC + code) * 2;
     const double2 a = c[0], b = c[1];
     v[0] = a.x;
     v[1] = a.y;
@@ -240,8 +267,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
   auto stage_ct = [&](double2* d, int node) {
     const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp16_tab(d + c * 32 + lane, gs + c * 32);
+    for (int c = 0; c < (TBLC + 31) / 32; ++c)
+      if (c * 32 + lane < TBLC) cp16_tab(d + c * 32 + lane, gs + c * 32);
   };
+  static_assert(!CH || (TBLC <= SD2 && TCC + TBLC <= SD2), "an e_k table fits slot Q and the tail of slot B");
   // the whole cherry block (table, the tips' TC blocks, their node ids)
   auto stage_cb = [&](double2* d, int node) {
     const double2* gs = reinterpret_cast<const double2*>(PS.ct) + size_t(node - N - 1) * kCherryBlk + lane;

@@ -345,3 +345,32 @@ def test_walk4s_cherry_tables(shape, branch_q, monkeypatch):
     monkeypatch.setenv("PG_WALK4S_CHERRY", "1")
     eng, ref = (_instance_pair(inst) if nw is None else _newick_pair(nw, 30000, 17))
     assert_logl(eng.log_likelihood(), ref.branch_gradient(False)[0])
+
+
+@pytest.mark.parametrize("branch_q", [False, True], ids=["homog", "per_branch_q"])
+def test_walk4s_cherry_tables_with_missing_data(branch_q, monkeypatch):
+    """Data with missing characters (5-column TC blocks): the cherries' e_k
+    tables over the 25 code pairs (the cherry keeps its own pre-order step),
+    against the oracle and the table-free kernel, gradient and Hessian."""
+    inst = synth.generate("C2", seed=9, sites=40000, tips=96)
+    assert int(inst.codes.min()) < 0  # missing characters present
+    monkeypatch.setenv("PG_WALKL", "0")
+    monkeypatch.setenv("PG_WALK4_LCV", "4")
+    monkeypatch.setenv("PG_WALK4S", "1")
+    reps = {}
+    for ch in ("1", "0"):
+        monkeypatch.setenv("PG_WALK4S_CHERRY", ch)
+        eng, ref = _instance_pair(inst, _branch_q(3, inst.branches) if branch_q else ())
+        g_only = eng.branch_gradient(False)
+        assert eng.info()["kernel"] == "walk4s_kernel"
+        assert eng.info()["launches"] == (4 if ch == "1" else 3)
+        reps[ch] = (g_only, eng.branch_gradient(True))
+    ll, g, h = ref.branch_gradient(True)
+    for g_only, rep in reps.values():
+        assert_logl(rep.log_likelihood, ll)
+        assert_vec(g_only.branch_gradient, g)
+        assert_vec(rep.branch_gradient, g)
+        assert_vec(rep.hessian_diagonal, h, rtol=1e-8, what="hessian")
+    # unfused cherry steps: the same arithmetic as the table-free kernel
+    assert reps["1"][1].log_likelihood == reps["0"][1].log_likelihood
+    assert np.array_equal(reps["1"][1].branch_gradient, reps["0"][1].branch_gradient)
