@@ -107,6 +107,22 @@ struct Walk4SGeom {
 //    its own step.
 // A cherry block (kCherryBlk double2) is [e_k | TC_u | TC_v | ids | W_u | W_v].
 
+// Table layout: the 32 bytes of a (category, code pair) entry as two 16-byte
+// halves [category][half][code pair] (PG_W4S_CT_SOA, default) -- a lane's two
+// LDS.128 then fall into bank group (code pair mod 8) instead of (code pair
+// mod 4) of the entry-major layout, halving the gathers' bank conflicts.
+#ifndef PG_W4S_CT_SOA
+#define PG_W4S_CT_SOA 1
+#endif
+// double offset of element r of entry (l, combo) in a table of ncc code pairs
+__host__ __device__ constexpr int cherry_elem(int l, int combo, int r, int ncc) {
+#if PG_W4S_CT_SOA
+  return ((l * 2 + (r >> 1)) * ncc + combo) * 2 + (r & 1);
+#else
+  return (l * ncc + combo) * 4 + r;
+#endif
+}
+
 // one thread per (cherry, category, code pair); TC is [B][4][4][4]
 static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int ncherry, int N, const double* __restrict__ tc,
                                         const double* __restrict__ qtc, double* __restrict__ ct) {
@@ -132,12 +148,12 @@ static __global__ void cherry_tc_kernel(const int4* __restrict__ cherries, int n
     }
   }
   double* blk = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk);
-  double* out = blk + l * 64 + combo * 4;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    out[r] = e[r];
-    out[2 * 200 + r] = wu[r];
-    out[2 * 328 + r] = wv[r];
+    const int o = cherry_elem(l, combo, r, 16);
+    blk[o] = e[r];
+    blk[2 * 200 + o] = wu[r];
+    blk[2 * 328 + o] = wv[r];
   }
   // the tips' own TC blocks (32 double2 each) and node ids behind the table
   const int t64 = i & 63;
@@ -166,9 +182,9 @@ static __global__ void cherry_tc5_kernel(const int4* __restrict__ cherries, int 
 #pragma unroll
     for (int r = 0; r < 4; ++r) e[r] = fma(Tk[c * 4 + r], xc, e[r]);
   }
-  double* out = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk) + l * 100 + combo * 4;
+  double* blk = ct + size_t(ch.x - N - 1) * (2 * kCherryBlk);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) out[r] = e[r];
+  for (int r = 0; r < 4; ++r) blk[cherry_elem(l, combo, r, 25)] = e[r];
 }
 
 // combined code rows of the cherries: cc[k - N - 1][s] = nc code_a[s] + code_b[s]
@@ -257,8 +273,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CH ? PG_WALK4S_MINB_CH : 
   };
   // a cherry's table [category][code pair][4] staged in an operand slot
   auto gather_ct = [&](const double2* tbl, int code, int j, double (&v)[4]) {
+#if PG_W4S_CT_SOA
+    const double2 a = tbl[(j * 2) * NCC + code], b = tbl[(j * 2 + 1) * NCC + code];
+#else
     const double2* c = tbl + (j * NCC + code) * 2;
     const double2 a = c[0], b = c[1];
+#endif
     v[0] = a.x;
     v[1] = a.y;
     v[2] = b.x;
