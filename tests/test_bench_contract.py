@@ -57,6 +57,26 @@ def test_device_arm_json_line():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
+@pytest.mark.gpu
+def test_other_workloads_block():
+    """`--also` measures further configs in their own processes after the main
+    line (the default C3 run carries C2 / C4 / C5): here C2 next to a C1 line,
+    with its full-size parity fixture."""
+    out = subprocess.run([sys.executable, "bench.py", "--config", "C1", "--steps", "3", "--warmup", "3",
+                          "--no-cpu-baseline", "--also", "C2"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["config"]["workload"] == "C1"
+    (o,) = d["other_workloads"]
+    assert "error" not in o, o
+    assert o["workload"] == "C2" and o["patterns"] == 20000 and o["steps"] == 3
+    assert o["ms_per_step"] > 0 and o["value"] > 0 and o["e2e_value"] > 0 and o["gpu_launches"] == 9
+    assert o["roofline"]["bound"] == "hbm" and 0 < o["roofline"]["frac"] < 1.2
+    assert o["parity"]["fixture"] == "tests/golden/full_C2.npz" and o["parity"]["within_1e-9"] is True
+
+
 def test_both_arms_share_config_and_parity_block(tmp_path, monkeypatch):
     """Identical `config` in both arms; the parity block compares against a
     full-size fixture only when the instance digest matches."""
