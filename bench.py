@@ -191,6 +191,9 @@ def roofline_block(inst, patterns, walk_ms, kernel, world, config):
         dram = prof["dram_bytes_per_launch"] / t / 1e9
         roof.update({"traffic_source": prof.get("source"), "dram_achieved_gbps": dram, "dram_frac_of_hbm": dram / hbm,
                      "traffic_over_algorithmic": prof["dram_bytes_per_launch"] / balg})
+        if prof["dram_bytes_per_launch"] < balg:
+            roof["traffic_note"] = ("below the algorithmic bytes: the walk never materialises the edge messages of "
+                                    "cherries (tabulated per tip-code pair, DESIGN.md section 2.1)")
         for k in ("dmma_pipe_active_pct", "fp64_pipe_active_pct", "dram_throughput_pct_of_peak"):
             if k in prof:
                 roof["ncu_" + k] = prof[k]
